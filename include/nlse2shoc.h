@@ -1,0 +1,149 @@
+/* nlse2shoc.h — C-ABI of the B200 (sm_100a) RK4 + 2SHOC NLSE library (libnlse2shoc.so).
+ *
+ * The library integrates the nonlinear Schrodinger equation
+ *     i Psi_t + a Lap(Psi) - V(r) Psi + s |Psi|^2 Psi = 0          (PAPER.md `NLSE`)
+ * with the method of lines: classic fourth-order Runge-Kutta in time (`RK4`)
+ * and the two-step high-order compact (2SHOC) Laplacian in space:
+ *     step 1   D_d = delta_d^2 Psi                      (`2shoc1d`, `2d2shocMs1`, `3d2shocMs1`)
+ *     step 2   Lap = sum_d 7/6 D_d - (D_d(+e_d) + D_d(-e_d))/12
+ *                                                      (`2shoc1d2`, `2d2shocMs2`, `3d2shocMs2`)
+ * with the paper's boundary rule for the intermediate D (DESIGN.md
+ * readings R8/R9) and the Psi_t boundary condition (`dbc_ut`).
+ * PAPER.md = /root/reference/PAPER.md (read at build time only; P:n = line n).
+ *
+ * Conventions shared by every call
+ *  - Grid: dims in {1,2,3}; N[3] = point counts along (x, y, z) (unused axes: 1);
+ *    coordinate of index i along axis d is xmin[d] + i*h[d]; every index 0 and
+ *    N[d]-1 is a boundary point.  N[d] >= 5 on every used axis.
+ *  - Field layout: row-major [z][y][x], x fastest, complex interleaved (re, im): the memory
+ *    of a contiguous torch.complex64 / complex128 tensor of shape (Nz, Ny, Nx) (dims dropped
+ *    from the left for 1D/2D).  Sharded handles: the local z-slab [z0, z0+nz) only.
+ *  - Pointers marked "device" are CUDA device pointers on the handle's device, 16-byte
+ *    aligned, caller-owned (the library never frees them).
+ *  - Every call returns nlse2shoc_status (0 = OK, < 0 = error); nothing aborts.  Detail of
+ *    the last error on the calling thread: nlse2shoc_last_error().
+ *  - Work is enqueued on the caller's CUDA stream (cudaStream_t passed as void*; NULL = the
+ *    legacy default stream) and the call returns after enqueue, except where noted "syncs".
+ *    Asynchronous faults surface at the caller's next synchronisation.
+ *  - A handle is not thread-safe; distinct handles are independent.
+ */
+#ifndef NLSE2SHOC_H
+#define NLSE2SHOC_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct nlse2shoc_s *nlse2shoc_t;
+
+typedef enum {
+  NLSE2SHOC_OK = 0,
+  NLSE2SHOC_EINVAL = -1,       /* invalid argument (see each call)                       */
+  NLSE2SHOC_ENOMEM = -2,       /* device allocation failed                               */
+  NLSE2SHOC_ECUDA = -3,        /* CUDA runtime / driver error                            */
+  NLSE2SHOC_ENCCL = -4,        /* NCCL error (sharded handles)                           */
+  NLSE2SHOC_ENONFINITE = -5,   /* non-finite value found by nlse2shoc_check_finite       */
+  NLSE2SHOC_EUNSUPPORTED = -6  /* option not built (e.g. no NCCL in this build)          */
+} nlse2shoc_status;
+
+/* Boundary conditions.
+ *  DIRICHLET: Lap_b = lambda_b = -(s|Psi_b|^2 - V_b) Psi_b / a (`dbc_lap`) for step 1,
+ *             Psi_t,b = 0 exactly (`dbc_ut`).
+ *  LAPZERO:   "Laplacian-zero": lambda_b = 0, Psi_t,b = i (s|Psi_b|^2 - V_b) Psi_b
+ *             (reading R9).
+ * At a d-face point b (index_d in {0, N_d-1}, all other indices interior) the per-axis
+ * intermediate is D_d(b) = lambda_b - sum_{e != d} delta_e^2 Psi_b (reading R8).          */
+typedef enum { NLSE2SHOC_BC_DIRICHLET = 0, NLSE2SHOC_BC_LAPZERO = 1 } nlse2shoc_bc;
+
+typedef enum { NLSE2SHOC_C64 = 0, NLSE2SHOC_C128 = 1 } nlse2shoc_dtype;
+
+typedef enum { NLSE2SHOC_V_NONE = 0, NLSE2SHOC_V_HARMONIC = 1, NLSE2SHOC_V_ARRAY = 2 } nlse2shoc_vkind;
+
+/* Potential V(r) of `NLSE`.
+ *  NONE:      V = 0.
+ *  HARMONIC:  V = w[0](x-c[0])^2 + w[1](y-c[1])^2 + w[2](z-c[2])^2 (absent axes dropped),
+ *             x = xmin[0] + i h[0] etc.; evaluated on the fly from per-axis tables (no HBM
+ *             field).
+ *  ARRAY:     data = device pointer to N[0]*N[1]*N[2] (sharded: the local slab) real values
+ *             of the handle's precision (float for C64, double for C128) in the field layout;
+ *             borrowed: the caller keeps it alive and unchanged until destroy.
+ * xmin is also used by nothing else (coordinates only enter through V).                   */
+typedef struct {
+  nlse2shoc_vkind kind;
+  double xmin[3];
+  double w[3];
+  double c[3];
+  const void *data;
+} nlse2shoc_potential;
+
+/* Create a single-GPU handle on the current CUDA device.
+ *  out   : receives the handle (host pointer).
+ *  dims  : 1, 2 or 3.          N : counts (x, y, z), N[d] >= 5 for d < dims, 1 otherwise.
+ *  h     : spacing per axis, finite and > 0 (anisotropic allowed; R17).
+ *  a     : > 0, finite.  s : finite.  V : NULL means V_NONE.
+ *  bc, dtype : see enums.
+ * Allocates the workspace (3 fields for the fused RK4: two stage buffers and the RK4
+ * accumulator; see nlse2shoc_workspace_bytes).  EINVAL / ENOMEM / ECUDA.              */
+nlse2shoc_status nlse2shoc_create(nlse2shoc_t *out, int dims, const int64_t N[3], const double h[3],
+                                  double a, double s, const nlse2shoc_potential *V, nlse2shoc_bc bc,
+                                  nlse2shoc_dtype dtype);
+
+/* z-slab sharding (3D, and 2D along y) over nranks processes, one GPU each.
+ * N is GLOBAL; this rank owns the slowest-axis slab [z0, z0+nz) given by
+ * nlse2shoc_local_extent (even split, remainder to the first ranks; nz >= 2).  The
+ * caller's Psi / L / V.data are the LOCAL slab.  id128 is the 128-byte NCCL unique id that
+ * rank 0 obtained from nlse2shoc_get_unique_id and broadcast (e.g. with torch.distributed).
+ * Collective: every rank must call it, and afterwards every rank must make the same
+ * sequence of laplacian / rk4 / stability_bound calls with the same dt and nsteps
+ * (a mismatch deadlocks inside NCCL; not detected).  EUNSUPPORTED if built without NCCL. */
+nlse2shoc_status nlse2shoc_get_unique_id(void *id128);
+nlse2shoc_status nlse2shoc_create_sharded(nlse2shoc_t *out, int dims, const int64_t N[3], const double h[3],
+                                          double a, double s, const nlse2shoc_potential *V, nlse2shoc_bc bc,
+                                          nlse2shoc_dtype dtype, const void *id128, int rank, int nranks);
+/* Slab owned by this handle along the slowest axis (z in 3D, y in 2D, whole grid in 1D). */
+nlse2shoc_status nlse2shoc_local_extent(nlse2shoc_t, int64_t *z0, int64_t *nz);
+/* Split rule used by create_sharded (pure host function, no handle needed). */
+nlse2shoc_status nlse2shoc_split(int64_t n_slow, int nranks, int rank, int64_t *z0, int64_t *nz);
+
+/* Device bytes the handle allocated (workspace + halos + tables). */
+size_t nlse2shoc_workspace_bytes(nlse2shoc_t);
+
+/* 0 = FUSED (default): one kernel per RK4 stage computes the whole 2SHOC Laplacian (both
+ *     steps, D never stored), the RHS and the RK4 stage combine.
+ * 1 = TWO_KERNEL: the paper's single-storage scheme (`2d2shocs1/2`, `3d2shocs`):
+ *     kernel A stores D = sum_d delta_d^2 Psi (D_b = lambda_b), kernel B applies step 2 +
+ *     RHS + combine.  One more field of workspace (allocated on first use).
+ * EINVAL for other values.                                                             */
+nlse2shoc_status nlse2shoc_set_variant(nlse2shoc_t, int variant);
+
+/* L = Lap(psi) by 2SHOC; boundary points get L_b = lambda_b.  psi, L: device,
+ * field layout, distinct.  Sharded: halo exchange included (collective).             */
+nlse2shoc_status nlse2shoc_laplacian(nlse2shoc_t, const void *psi, void *L, void *stream);
+
+/* nsteps classic RK4 steps of size dt in place on psi (device, field layout).
+ * dt finite > 0, nsteps >= 0.  The result is the same polynomial as the paper's listing
+ * evaluated with a Psi-space accumulator.               */
+nlse2shoc_status nlse2shoc_rk4(nlse2shoc_t, void *psi, double dt, int64_t nsteps, void *stream);
+
+/* kmax of `kdfull` from psi (device): B = 0 (Table 1 Dirichlet; Laplacian-zero
+ * by reading R14), G of Table 2 via its closed form g in [-4d/12, 64d/12] (isotropic h);
+ * anisotropic h: reading R17.  Sharded: global over all ranks (collective).  Syncs. */
+nlse2shoc_status nlse2shoc_stability_bound(nlse2shoc_t, const void *psi, double *kmax, void *stream);
+
+/* Scan psi (device) for NaN/Inf; returns ENONFINITE if any is found.  Syncs. */
+nlse2shoc_status nlse2shoc_check_finite(nlse2shoc_t, const void *psi, void *stream);
+
+/* Number of CUDA kernels the last laplacian / rk4 call enqueued (instrumentation). */
+int64_t nlse2shoc_last_launch_count(nlse2shoc_t);
+
+const char *nlse2shoc_strerror(nlse2shoc_status);
+const char *nlse2shoc_last_error(void);
+/* Library version string, e.g. "nlse2shoc 0.1 sm_100a nccl". */
+const char *nlse2shoc_version(void);
+void nlse2shoc_destroy(nlse2shoc_t);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

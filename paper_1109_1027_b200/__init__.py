@@ -1,0 +1,186 @@
+"""paper_1109_1027_b200 — B200-native RK4 + 2SHOC NLSE step (arxiv 1109.1027).
+
+Thin Python binding over the C-ABI of ``libnlse2shoc.so`` (include/nlse2shoc.h).  The
+functions below carry the C names and only marshal arguments (torch tensors -> device
+pointers, the current CUDA stream -> cudaStream_t); every step of the path runs in the
+library's sm_100a kernels.  PyTorch provides device memory, streams and process groups.
+"""
+from __future__ import annotations
+
+import ctypes
+
+from ._lib import BC, DTYPE, VKIND, NLSE2SHOCError, Potential, check, lib
+
+__all__ = [
+    "Solver", "NLSE2SHOCError", "nlse2shoc_create", "nlse2shoc_create_sharded", "nlse2shoc_get_unique_id",
+    "nlse2shoc_laplacian", "nlse2shoc_rk4", "nlse2shoc_stability_bound", "nlse2shoc_check_finite",
+    "nlse2shoc_split", "nlse2shoc_version", "solver_from_work",
+]
+
+
+def _stream(stream):
+    import torch
+
+    if stream is None:
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _potential(V, dims):
+    p = Potential()
+    keep = None
+    if V is None or V.get("kind", "none") == "none":
+        p.kind = VKIND["none"]
+        return p, keep
+    p.kind = VKIND[V["kind"]]
+    for d in range(3):
+        p.xmin[d] = float(V.get("xmin", [0.0] * 3)[d]) if d < len(V.get("xmin", [])) else 0.0
+        p.w[d] = float(V.get("w", [0.0] * 3)[d]) if d < len(V.get("w", [])) else 0.0
+        p.c[d] = float(V.get("c", [0.0] * 3)[d]) if d < len(V.get("c", [])) else 0.0
+    if V["kind"] == "array":
+        keep = V["data"]  # torch tensor on the device; kept alive by the Solver
+        p.data = keep.data_ptr()
+    return p, keep
+
+
+def nlse2shoc_version() -> str:
+    return lib().nlse2shoc_version().decode()
+
+
+def nlse2shoc_split(n_slow: int, nranks: int, rank: int):
+    z0, nz = ctypes.c_int64(), ctypes.c_int64()
+    check(lib().nlse2shoc_split(int(n_slow), int(nranks), int(rank), ctypes.byref(z0), ctypes.byref(nz)), "split")
+    return z0.value, nz.value
+
+
+def nlse2shoc_get_unique_id() -> bytes:
+    buf = (ctypes.c_ubyte * 128)()
+    check(lib().nlse2shoc_get_unique_id(buf), "get_unique_id")
+    return bytes(buf)
+
+
+def _args(dims, N, h):
+    n = [int(v) for v in list(N)[:dims]] + [1] * (3 - dims)
+    hh = [float(v) for v in list(h)[:dims]] + [1.0] * (3 - dims)
+    return (ctypes.c_int64 * 3)(*n), (ctypes.c_double * 3)(*hh)
+
+
+def nlse2shoc_create(dims, N, h, a, s, V=None, bc="dirichlet", dtype="c64"):
+    H = ctypes.c_void_p()
+    n, hh = _args(dims, N, h)
+    pv, keep = _potential(V, dims)
+    check(lib().nlse2shoc_create(ctypes.byref(H), int(dims), n, hh, float(a), float(s), ctypes.byref(pv), BC[bc],
+                                 DTYPE[dtype]), "create")
+    return H, keep
+
+
+def nlse2shoc_create_sharded(dims, N, h, a, s, V, bc, dtype, uid: bytes, rank: int, nranks: int):
+    H = ctypes.c_void_p()
+    n, hh = _args(dims, N, h)
+    pv, keep = _potential(V, dims)
+    buf = (ctypes.c_ubyte * 128).from_buffer_copy(uid)
+    check(lib().nlse2shoc_create_sharded(ctypes.byref(H), int(dims), n, hh, float(a), float(s), ctypes.byref(pv),
+                                         BC[bc], DTYPE[dtype], buf, int(rank), int(nranks)), "create_sharded")
+    return H, keep
+
+
+def nlse2shoc_laplacian(H, psi, L, stream=None):
+    check(lib().nlse2shoc_laplacian(H, _ptr(psi), _ptr(L), _stream(stream)), "laplacian")
+    return L
+
+
+def nlse2shoc_rk4(H, psi, dt, nsteps, stream=None):
+    check(lib().nlse2shoc_rk4(H, _ptr(psi), float(dt), int(nsteps), _stream(stream)), "rk4")
+    return psi
+
+
+def nlse2shoc_stability_bound(H, psi, stream=None) -> float:
+    k = ctypes.c_double()
+    check(lib().nlse2shoc_stability_bound(H, _ptr(psi), ctypes.byref(k), _stream(stream)), "stability_bound")
+    return k.value
+
+
+def nlse2shoc_check_finite(H, psi, stream=None):
+    check(lib().nlse2shoc_check_finite(H, _ptr(psi), _stream(stream)), "check_finite")
+
+
+class Solver:
+    """Owns one nlse2shoc handle.  Psi tensors are contiguous torch complex64/complex128
+    CUDA tensors of shape (Nz, Ny, Nx) / (Ny, Nx) / (Nx,) (sharded: the local slab)."""
+
+    def __init__(self, dims, N, h, a, s, V=None, bc="dirichlet", dtype="c64", shard=None):
+        self.dims, self.dtype, self.bc = int(dims), dtype, bc
+        self.N = [int(v) for v in list(N)[:dims]]
+        if shard is None:
+            self._h, self._keep = nlse2shoc_create(dims, N, h, a, s, V, bc, dtype)
+        else:
+            self._h, self._keep = nlse2shoc_create_sharded(dims, N, h, a, s, V, bc, dtype, shard["uid"],
+                                                           shard["rank"], shard["nranks"])
+        z0, nz = ctypes.c_int64(), ctypes.c_int64()
+        check(lib().nlse2shoc_local_extent(self._h, ctypes.byref(z0), ctypes.byref(nz)), "local_extent")
+        self.z0, self.nz = z0.value, nz.value
+
+    @property
+    def local_shape(self):
+        if self.dims == 1:
+            return (self.N[0],)
+        if self.dims == 2:
+            return (self.nz, self.N[0])
+        return (self.nz, self.N[1], self.N[0])
+
+    def set_variant(self, variant: int):
+        check(lib().nlse2shoc_set_variant(self._h, int(variant)), "set_variant")
+
+    def laplacian(self, psi, out=None, stream=None):
+        import torch
+
+        if out is None:
+            out = torch.empty_like(psi)
+        return nlse2shoc_laplacian(self._h, psi, out, stream)
+
+    def rk4(self, psi, dt, nsteps, stream=None):
+        return nlse2shoc_rk4(self._h, psi, dt, nsteps, stream)
+
+    def stability_bound(self, psi, stream=None) -> float:
+        return nlse2shoc_stability_bound(self._h, psi, stream)
+
+    def check_finite(self, psi, stream=None):
+        nlse2shoc_check_finite(self._h, psi, stream)
+
+    @property
+    def workspace_bytes(self) -> int:
+        return int(lib().nlse2shoc_workspace_bytes(self._h))
+
+    @property
+    def last_launch_count(self) -> int:
+        return int(lib().nlse2shoc_last_launch_count(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().nlse2shoc_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def solver_from_work(work: dict, dtype: str, V_array=None, shard=None) -> Solver:
+    """Solver for a workload dict (icgen.configs layout: grid, a, s, V, bc).  ``V_array`` is
+    the device tensor for V kind 'array'."""
+    g = work["grid"]
+    dims = g["dims"]
+    V = dict(work["V"])
+    if V["kind"] in ("harmonic", "array"):
+        V["xmin"] = list(g["xmin"])
+    if V["kind"] == "array":
+        V["data"] = V_array
+    return Solver(dims, g["n"][:dims], g["h"][:dims], work["a"], work["s"], V, work["bc"], dtype, shard=shard)

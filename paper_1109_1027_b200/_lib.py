@@ -1,0 +1,101 @@
+"""ctypes declarations of the C-ABI in include/nlse2shoc.h (argument marshalling only).
+
+Loading fails loudly if libnlse2shoc.so is missing: there is no CPU or Python fallback for
+any step of the path.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(_HERE, "libnlse2shoc.so")
+
+OK, EINVAL, ENOMEM, ECUDA, ENCCL, ENONFINITE, EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
+BC = {"dirichlet": 0, "lapzero": 1}
+DTYPE = {"c64": 0, "c128": 1}
+VKIND = {"none": 0, "harmonic": 1, "array": 2}
+
+
+class Potential(ctypes.Structure):
+    _fields_ = [
+        ("kind", ctypes.c_int),
+        ("xmin", ctypes.c_double * 3),
+        ("w", ctypes.c_double * 3),
+        ("c", ctypes.c_double * 3),
+        ("data", ctypes.c_void_p),
+    ]
+
+
+class NLSE2SHOCError(RuntimeError):
+    def __init__(self, status, where, detail):
+        super().__init__(f"{where}: status {status} ({detail})")
+        self.status = status
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(SO_PATH):
+            raise ImportError(
+                f"{SO_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(nvcc, sm_100a).  There is no fallback implementation."
+            )
+        L = ctypes.CDLL(SO_PATH)
+        H = ctypes.c_void_p
+        i64p = ctypes.POINTER(ctypes.c_int64)
+        dbl3 = ctypes.c_double * 3
+        i643 = ctypes.c_int64 * 3
+        sig = {
+            "nlse2shoc_create": [ctypes.POINTER(H), ctypes.c_int, i643, dbl3, ctypes.c_double, ctypes.c_double,
+                                 ctypes.POINTER(Potential), ctypes.c_int, ctypes.c_int],
+            "nlse2shoc_get_unique_id": [ctypes.c_void_p],
+            "nlse2shoc_create_sharded": [ctypes.POINTER(H), ctypes.c_int, i643, dbl3, ctypes.c_double, ctypes.c_double,
+                                         ctypes.POINTER(Potential), ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                         ctypes.c_int, ctypes.c_int],
+            "nlse2shoc_local_extent": [H, i64p, i64p],
+            "nlse2shoc_split": [ctypes.c_int64, ctypes.c_int, ctypes.c_int, i64p, i64p],
+            "nlse2shoc_set_variant": [H, ctypes.c_int],
+            "nlse2shoc_laplacian": [H, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p],
+            "nlse2shoc_rk4": [H, ctypes.c_void_p, ctypes.c_double, ctypes.c_int64, ctypes.c_void_p],
+            "nlse2shoc_stability_bound": [H, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_void_p],
+            "nlse2shoc_check_finite": [H, ctypes.c_void_p, ctypes.c_void_p],
+        }
+        for name, args in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = ctypes.c_int
+        L.nlse2shoc_workspace_bytes.argtypes = [H]
+        L.nlse2shoc_workspace_bytes.restype = ctypes.c_size_t
+        L.nlse2shoc_last_launch_count.argtypes = [H]
+        L.nlse2shoc_last_launch_count.restype = ctypes.c_int64
+        L.nlse2shoc_strerror.argtypes = [ctypes.c_int]
+        L.nlse2shoc_strerror.restype = ctypes.c_char_p
+        L.nlse2shoc_last_error.argtypes = []
+        L.nlse2shoc_last_error.restype = ctypes.c_char_p
+        L.nlse2shoc_version.argtypes = []
+        L.nlse2shoc_version.restype = ctypes.c_char_p
+        L.nlse2shoc_destroy.argtypes = [H]
+        L.nlse2shoc_destroy.restype = None
+        _lib = L
+    return _lib
+
+
+def check(status, where):
+    if status != OK:
+        L = lib()
+        raise NLSE2SHOCError(status, where, (L.nlse2shoc_strerror(status).decode() + ": "
+                                             + L.nlse2shoc_last_error().decode()))
+    return status
+
+
+# Header symbols, for the "library exports everything include/*.h declares" test.
+EXPORTS = [
+    "nlse2shoc_create", "nlse2shoc_get_unique_id", "nlse2shoc_create_sharded", "nlse2shoc_local_extent",
+    "nlse2shoc_split", "nlse2shoc_workspace_bytes", "nlse2shoc_set_variant", "nlse2shoc_laplacian",
+    "nlse2shoc_rk4", "nlse2shoc_stability_bound", "nlse2shoc_check_finite", "nlse2shoc_last_launch_count",
+    "nlse2shoc_strerror", "nlse2shoc_last_error", "nlse2shoc_version", "nlse2shoc_destroy",
+]

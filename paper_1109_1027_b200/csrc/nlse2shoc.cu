@@ -1,0 +1,792 @@
+// nlse2shoc.cu — host runtime of libnlse2shoc.so: the C-ABI declared in include/nlse2shoc.h
+// (handle, validation, workspace, TMA descriptors, launch plan, NCCL z-slab halo exchange)
+// plus the kernel instantiations.  Product code: shares nothing with oracle/ or icgen/.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "nlse2shoc.h"
+#include "stage_line.cuh"
+#include "stage_stream.cuh"
+#include "two_kernel.cuh"
+
+#ifdef NLSE_WITH_NCCL
+#include <nccl.h>
+#endif
+
+using namespace nlse;
+
+// ------------------------------------------------------------------------------- errors
+static thread_local std::string g_last_error;
+
+static nlse2shoc_status fail(nlse2shoc_status st, const std::string &msg) {
+  g_last_error = msg;
+  return st;
+}
+#define CUDA_TRY(expr)                                                                        \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(e_ == cudaErrorMemoryAllocation ? NLSE2SHOC_ENOMEM : NLSE2SHOC_ECUDA,       \
+                  std::string(#expr) + ": " + cudaGetErrorString(e_));                        \
+  } while (0)
+#define TRY(expr)                                \
+  do {                                           \
+    nlse2shoc_status s_ = (expr);                \
+    if (s_ != NLSE2SHOC_OK) return s_;           \
+  } while (0)
+#ifdef NLSE_WITH_NCCL
+#define NCCL_TRY(expr)                                                                               \
+  do {                                                                                               \
+    ncclResult_t r_ = (expr);                                                                        \
+    if (r_ != ncclSuccess) return fail(NLSE2SHOC_ENCCL, std::string(#expr) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+#endif
+
+// --------------------------------------------------------------------------- TMA encode
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void *p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// ------------------------------------------------------------------------------ handle
+struct Field {  // one pitched field of the local slab (+ its two halo buffers when sharded)
+  void *ptr = nullptr;
+  void *halo_lo = nullptr, *halo_hi = nullptr;
+  CUtensorMap tm{}, tm_lo{}, tm_hi{};
+};
+
+struct nlse2shoc_s {
+  int dims = 0;
+  int64_t N[3] = {1, 1, 1};  // global counts
+  double h[3] = {1, 1, 1};
+  double a = 1, s = 0;
+  nlse2shoc_potential V{};
+  int bc = 0, dtype = 0, device = 0, variant = 0;
+  size_t S = 8;  // bytes per complex
+  // slab (streamed axis = dims-1)
+  int rank = 0, nranks = 1;
+  int64_t z0 = 0, nz = 1;   // local slab along the streamed axis
+  int64_t nx = 1, ny = 1;   // kernel view: x, y (3D only; 1 otherwise)
+  int64_t NZ = 1;           // global streamed count
+  int64_t pitch = 0, plane = 0, local_elems = 0;
+  bool sharded = false;
+  // workspace
+  Field psiw, TA, TB, acc, D;
+  void *vtab = nullptr;  // vx | vy | vz tables (precision R)
+  size_t vx_off = 0, vy_off = 0, vz_off = 0;
+  double *red = nullptr;  // reduction partials (device)
+  int red_blocks = 0;
+  size_t bytes = 0;
+  int num_sms = 148;
+  int64_t launches = 0;
+#ifdef NLSE_WITH_NCCL
+  ncclComm_t comm = nullptr;
+#endif
+};
+
+static const char *kErr[] = {"ok", "invalid argument", "out of device memory", "CUDA error", "NCCL error",
+                             "non-finite value", "unsupported"};
+
+// ------------------------------------------------------------------------ small helpers
+static bool finite_pos(double v) { return std::isfinite(v) && v > 0.0; }
+
+static nlse2shoc_status encode_map(CUtensorMap *tm, void *base, int dims_tensor, uint64_t inner_elems8,
+                                   uint64_t rows, uint64_t planes, uint64_t pitch_bytes, uint64_t plane_bytes,
+                                   uint32_t box0, uint32_t box1) {
+  auto enc = get_encode();
+  if (!enc) return fail(NLSE2SHOC_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t gdim[3] = {inner_elems8, rows, planes};
+  cuuint64_t gstr[2] = {pitch_bytes, plane_bytes};
+  cuuint32_t box[3] = {box0, box1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, dims_tensor, base, gdim, gstr, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(NLSE2SHOC_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  return NLSE2SHOC_OK;
+}
+
+template <int DIMS, typename R> struct Maps {
+  using LY = Layout<DIMS, R>;
+  using C = Cfg<DIMS, R>;
+  // stencil-input map (tile + halo box) over a field with `planes` planes
+  static nlse2shoc_status stencil(nlse2shoc_t H, CUtensorMap *tm, void *base, int64_t planes) {
+    const uint64_t S = sizeof(cplx<R>);
+    if (DIMS == 3)
+      return encode_map(tm, base, 3, uint64_t(H->nx) * LY::EPC, uint64_t(H->ny), uint64_t(planes), H->pitch * S,
+                        H->plane * S, LY::BW, LY::SROWS);
+    return encode_map(tm, base, 2, uint64_t(H->nx) * LY::EPC, uint64_t(planes), 1, H->pitch * S, H->pitch * S * planes,
+                      LY::BW, 1);
+  }
+  // pointwise (Psi^n / acc) map: tile box without halo
+  static nlse2shoc_status point(nlse2shoc_t H, CUtensorMap *tm, void *base) {
+    const uint64_t S = sizeof(cplx<R>);
+    if (DIMS == 3)
+      return encode_map(tm, base, 3, uint64_t(H->nx) * LY::EPC, uint64_t(H->ny), uint64_t(H->nz), H->pitch * S,
+                        H->plane * S, LY::BWP, C::TY);
+    return encode_map(tm, base, 2, uint64_t(H->nx) * LY::EPC, uint64_t(H->nz), 1, H->pitch * S, H->plane * S * H->nz,
+                      LY::BWP, 1);
+  }
+};
+
+template <typename R> static void fill_params(nlse2shoc_t H, StageParams<R> &P) {
+  std::memset(&P, 0, sizeof(P));
+  P.nx = int(H->nx);
+  P.ny = int(H->ny);
+  P.nz = int(H->nz);
+  P.z0 = int(H->z0);
+  P.NZ = int(H->NZ);
+  P.lo_face = H->z0 == 0;
+  P.hi_face = H->z0 + H->nz == H->NZ;
+  P.has_lo_halo = H->dims > 1 && !P.lo_face;
+  P.has_hi_halo = H->dims > 1 && !P.hi_face;
+  P.pitch = H->pitch;
+  P.plane = H->plane;
+  // physical spacing of kernel axes: x = axis 0; y = axis 1 (3D); streamed = axis dims-1
+  const double hx = H->h[0], hy = H->dims == 3 ? H->h[1] : 1.0, hz = H->dims >= 2 ? H->h[H->dims - 1] : 1.0;
+  P.cx = R(1.0 / (12.0 * hx * hx));
+  P.cy = R(1.0 / (12.0 * hy * hy));
+  P.cz = R(1.0 / (12.0 * hz * hz));
+  P.ihx2 = R(1.0 / (hx * hx));
+  P.ihy2 = R(1.0 / (hy * hy));
+  P.ihz2 = R(1.0 / (hz * hz));
+  P.hx2 = R(hx * hx);
+  P.hy2 = R(hy * hy);
+  P.hz2 = R(hz * hz);
+  P.a = R(H->a);
+  P.s = R(H->s);
+  P.inv_a = R(1.0 / H->a);
+  P.bc = H->bc;
+  P.vkind = int(H->V.kind);
+  if (H->V.kind == NLSE2SHOC_V_HARMONIC) {
+    const R *t = reinterpret_cast<const R *>(H->vtab);
+    P.vx = t + H->vx_off;
+    P.vy = H->dims == 3 ? t + H->vy_off : nullptr;
+    P.vz = H->dims >= 2 ? t + H->vz_off : nullptr;
+  }
+  if (H->V.kind == NLSE2SHOC_V_ARRAY) P.varr = reinterpret_cast<const R *>(H->V.data);
+}
+
+// ------------------------------------------------------------------------ launch plans
+template <int DIMS, typename R, int MODE> static nlse2shoc_status set_smem_attr() {
+  static bool done = false;
+  if (!done) {
+    CUDA_TRY(cudaFuncSetAttribute(stage_stream_kernel<DIMS, R, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(Layout<DIMS, R>::template smem_bytes<MODE>())));
+    done = true;
+  }
+  return NLSE2SHOC_OK;
+}
+
+template <int DIMS, typename R, int MODE>
+static nlse2shoc_status launch_stream(nlse2shoc_t H, Field &in, const CUtensorMap *tm_psi, const CUtensorMap *tm_acc,
+                                      StageParams<R> P, cudaStream_t st) {
+  using C = Cfg<DIMS, R>;
+  using LY = Layout<DIMS, R>;
+  TRY((set_smem_attr<DIMS, R, MODE>()));
+  const size_t smem = LY::template smem_bytes<MODE>();
+  int occ = 1;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stage_stream_kernel<DIMS, R, MODE>, LY::NTHREADS, smem));
+  occ = std::max(occ, 1);
+  const int G0 = H->num_sms * occ;
+  P.ncx = int((H->nx + C::TX - 1) / C::TX);
+  P.ncy = DIMS == 3 ? int((H->ny + C::TY - 1) / C::TY) : 1;
+  const int ncol = P.ncx * P.ncy;
+  // z-chunks: minimise rounds * (chunk length + priming cost)
+  int best = 1;
+  double bestc = 1e300;
+  for (int nc = 1; nc <= 16 && nc <= H->nz; ++nc) {
+    const double rounds = std::ceil(double(ncol) * nc / G0);
+    const double len = std::ceil(double(H->nz) / nc) + 1.5;
+    const double c = rounds * len;
+    if (c < bestc - 1e-9) { bestc = c; best = nc; }
+  }
+  P.nchunk = best;
+  P.ntiles = ncol * best;
+  const int G = std::min(G0, P.ntiles);
+  const CUtensorMap *lo = P.has_lo_halo ? &in.tm_lo : &in.tm;
+  const CUtensorMap *hi = P.has_hi_halo ? &in.tm_hi : &in.tm;
+  stage_stream_kernel<DIMS, R, MODE><<<G, LY::NTHREADS, smem, st>>>(in.tm, *lo, *hi, tm_psi ? *tm_psi : in.tm,
+                                                                   tm_acc ? *tm_acc : in.tm, P);
+  CUDA_TRY(cudaGetLastError());
+  ++H->launches;
+  return NLSE2SHOC_OK;
+}
+
+template <typename R, int MODE>
+static nlse2shoc_status launch_line(nlse2shoc_t H, const void *in, const void *psi, const void *acc, StageParams<R> P,
+                                    cudaStream_t st) {
+  const int threads = 256;
+  const int64_t blocks = std::min<int64_t>((H->nx + threads - 1) / threads, int64_t(H->num_sms) * 8);
+  stage_line_kernel<R, MODE><<<int(blocks), threads, 0, st>>>(
+      reinterpret_cast<const cplx<R> *>(in), reinterpret_cast<const cplx<R> *>(psi),
+      reinterpret_cast<const cplx<R> *>(acc), P);
+  CUDA_TRY(cudaGetLastError());
+  ++H->launches;
+  return NLSE2SHOC_OK;
+}
+
+// ------------------------------------------------------------------------- halo (NCCL)
+static nlse2shoc_status halo_exchange(nlse2shoc_t H, Field &f, cudaStream_t st) {
+  if (!H->sharded || H->nranks == 1) return NLSE2SHOC_OK;
+#ifdef NLSE_WITH_NCCL
+  const size_t bytes = size_t(2 * H->plane) * H->S;
+  char *base = reinterpret_cast<char *>(f.ptr);
+  NCCL_TRY(ncclGroupStart());
+  if (H->rank > 0) {
+    NCCL_TRY(ncclSend(base, bytes, ncclChar, H->rank - 1, H->comm, st));
+    NCCL_TRY(ncclRecv(f.halo_lo, bytes, ncclChar, H->rank - 1, H->comm, st));
+  }
+  if (H->rank < H->nranks - 1) {
+    NCCL_TRY(ncclSend(base + size_t(H->nz - 2) * H->plane * H->S, bytes, ncclChar, H->rank + 1, H->comm, st));
+    NCCL_TRY(ncclRecv(f.halo_hi, bytes, ncclChar, H->rank + 1, H->comm, st));
+  }
+  NCCL_TRY(ncclGroupEnd());
+  return NLSE2SHOC_OK;
+#else
+  (void)f;
+  (void)st;
+  return fail(NLSE2SHOC_EUNSUPPORTED, "built without NCCL");
+#endif
+}
+
+template <int DIMS, typename R>
+static nlse2shoc_status launch_two(int, int stage, const cplx<R> *in, const cplx<R> *lo, const cplx<R> *hi,
+                                   const cplx<R> *psi, const cplx<R> *acc, cplx<R> *D, const StageParams<R> &P,
+                                   const TwoParams<R> &Q, cudaStream_t st, int64_t &launches) {
+  CUDA_TRY((launch_two_impl<DIMS, R>(stage, in, lo, hi, psi, acc, D, P, Q, st)));
+  launches += 2;
+  return NLSE2SHOC_OK;
+}
+
+// ----------------------------------------------------------------------- stage drivers
+// Fused RK4: stage s reads X_{s-1} (stencil) and writes the next stage input + acc.
+template <int DIMS, typename R>
+static nlse2shoc_status rk4_fused(nlse2shoc_t H, Field &psi, double dt, int64_t nsteps, cudaStream_t st) {
+  StageParams<R> P;
+  fill_params<R>(H, P);
+  cplx<R> *pPsi = reinterpret_cast<cplx<R> *>(psi.ptr), *pA = reinterpret_cast<cplx<R> *>(H->TA.ptr),
+          *pB = reinterpret_cast<cplx<R> *>(H->TB.ptr), *pAcc = reinterpret_cast<cplx<R> *>(H->acc.ptr);
+  CUtensorMap tm_psi{}, tm_acc{};
+  if constexpr (DIMS >= 2) {
+    TRY((Maps<DIMS, R>::point(H, &tm_psi, psi.ptr)));
+    TRY((Maps<DIMS, R>::point(H, &tm_acc, H->acc.ptr)));
+  }
+  const R k = R(dt);
+  for (int64_t n = 0; n < nsteps; ++n) {
+    // stage 1: K1 = F(Psi^n); acc = Psi^n + k/6 K1; T_A = Psi^n + k/2 K1
+    TRY(halo_exchange(H, psi, st));
+    P.ca = R(dt / 6.0); P.cb = R(dt / 2.0); P.out_T = pA; P.out_acc = pAcc;
+    if constexpr (DIMS == 1) TRY((launch_line<R, M_S1>(H, pPsi, pPsi, pAcc, P, st)));
+    else TRY((launch_stream<DIMS, R, M_S1>(H, psi, nullptr, nullptr, P, st)));
+    // stage 2: K2 = F(T_A); acc += k/3 K2; T_B = Psi^n + k/2 K2
+    TRY(halo_exchange(H, H->TA, st));
+    P.ca = R(dt / 3.0); P.cb = R(dt / 2.0); P.out_T = pB; P.out_acc = pAcc;
+    if constexpr (DIMS == 1) TRY((launch_line<R, M_S2>(H, pA, pPsi, pAcc, P, st)));
+    else TRY((launch_stream<DIMS, R, M_S2>(H, H->TA, &tm_psi, &tm_acc, P, st)));
+    // stage 3: K3 = F(T_B); acc += k/3 K3; T_A = Psi^n + k K3
+    TRY(halo_exchange(H, H->TB, st));
+    P.ca = R(dt / 3.0); P.cb = k; P.out_T = pA; P.out_acc = pAcc;
+    if constexpr (DIMS == 1) TRY((launch_line<R, M_S3>(H, pB, pPsi, pAcc, P, st)));
+    else TRY((launch_stream<DIMS, R, M_S3>(H, H->TB, &tm_psi, &tm_acc, P, st)));
+    // stage 4: K4 = F(T_A); Psi^{n+1} = acc + k/6 K4 (pointwise, in place over Psi^n)
+    TRY(halo_exchange(H, H->TA, st));
+    P.ca = R(0); P.cb = R(dt / 6.0); P.out_T = pPsi; P.out_acc = nullptr;
+    if constexpr (DIMS == 1) TRY((launch_line<R, M_S4>(H, pA, pPsi, pAcc, P, st)));
+    else TRY((launch_stream<DIMS, R, M_S4>(H, H->TA, nullptr, &tm_acc, P, st)));
+  }
+  return NLSE2SHOC_OK;
+}
+
+template <int DIMS, typename R> static nlse2shoc_status lap_fused(nlse2shoc_t H, Field &psi, void *L, cudaStream_t st) {
+  StageParams<R> P;
+  fill_params<R>(H, P);
+  P.out_T = reinterpret_cast<cplx<R> *>(L);
+  TRY(halo_exchange(H, psi, st));
+  if constexpr (DIMS == 1) return launch_line<R, M_LAP>(H, psi.ptr, psi.ptr, psi.ptr, P, st);
+  else return launch_stream<DIMS, R, M_LAP>(H, psi, nullptr, nullptr, P, st);
+}
+
+// Two-kernel (single-storage D in HBM, PAPER.md `2d2shocs1/2`, `3d2shocs`) RK4.
+template <int DIMS, typename R>
+static nlse2shoc_status rk4_two(nlse2shoc_t H, Field &psi, double dt, int64_t nsteps, cudaStream_t st) {
+  StageParams<R> P;
+  fill_params<R>(H, P);
+  TwoParams<R> Q;
+  two_params<R>(H->dims, H->h, Q);
+  cplx<R> *pPsi = reinterpret_cast<cplx<R> *>(psi.ptr), *pA = reinterpret_cast<cplx<R> *>(H->TA.ptr),
+          *pB = reinterpret_cast<cplx<R> *>(H->TB.ptr), *pAcc = reinterpret_cast<cplx<R> *>(H->acc.ptr),
+          *pD = reinterpret_cast<cplx<R> *>(H->D.ptr);
+  Field *ins[4] = {&psi, &H->TA, &H->TB, &H->TA};
+  cplx<R> *outs[4] = {pA, pB, pA, pPsi};
+  const double ca[4] = {dt / 6.0, dt / 3.0, dt / 3.0, 0.0}, cb[4] = {dt / 2.0, dt / 2.0, dt, dt / 6.0};
+  for (int64_t n = 0; n < nsteps; ++n) {
+    for (int s = 0; s < 4; ++s) {
+      TRY(halo_exchange(H, *ins[s], st));
+      P.ca = R(ca[s]);
+      P.cb = R(cb[s]);
+      P.out_T = outs[s];
+      P.out_acc = s < 3 ? pAcc : nullptr;
+      const cplx<R> *in = reinterpret_cast<const cplx<R> *>(ins[s]->ptr);
+      const cplx<R> *lo = reinterpret_cast<const cplx<R> *>(ins[s]->halo_lo);
+      const cplx<R> *hi = reinterpret_cast<const cplx<R> *>(ins[s]->halo_hi);
+      TRY((launch_two<DIMS, R>(H->num_sms, s + 1, in, lo, hi, pPsi, pAcc, pD, P, Q, st, H->launches)));
+    }
+  }
+  return NLSE2SHOC_OK;
+}
+
+template <int DIMS, typename R> static nlse2shoc_status lap_two(nlse2shoc_t H, Field &psi, void *L, cudaStream_t st) {
+  StageParams<R> P;
+  fill_params<R>(H, P);
+  TwoParams<R> Q;
+  two_params<R>(H->dims, H->h, Q);
+  P.out_T = reinterpret_cast<cplx<R> *>(L);
+  TRY(halo_exchange(H, psi, st));
+  const cplx<R> *in = reinterpret_cast<const cplx<R> *>(psi.ptr);
+  return launch_two<DIMS, R>(H->num_sms, 5, in, reinterpret_cast<const cplx<R> *>(psi.halo_lo),
+                             reinterpret_cast<const cplx<R> *>(psi.halo_hi), nullptr, nullptr,
+                             reinterpret_cast<cplx<R> *>(H->D.ptr), P, Q, st, H->launches);
+}
+
+// ------------------------------------------------------------------------------ create
+static nlse2shoc_status alloc_field(nlse2shoc_t H, Field &f, bool halos) {
+  const size_t bytes = size_t(H->local_elems) * H->S;
+  CUDA_TRY(cudaMalloc(&f.ptr, bytes));
+  H->bytes += bytes;
+  if (halos && H->sharded) {
+    const size_t hb = size_t(2 * H->plane) * H->S;
+    CUDA_TRY(cudaMalloc(&f.halo_lo, hb));
+    CUDA_TRY(cudaMalloc(&f.halo_hi, hb));
+    CUDA_TRY(cudaMemsetAsync(f.halo_lo, 0, hb));
+    CUDA_TRY(cudaMemsetAsync(f.halo_hi, 0, hb));
+    H->bytes += 2 * hb;
+  }
+  return NLSE2SHOC_OK;
+}
+
+template <typename R> static nlse2shoc_status encode_field_maps(nlse2shoc_t H, Field &f) {
+  if (H->dims == 3) {
+    TRY((Maps<3, R>::stencil(H, &f.tm, f.ptr, H->nz)));
+    if (f.halo_lo) TRY((Maps<3, R>::stencil(H, &f.tm_lo, f.halo_lo, 2)));
+    if (f.halo_hi) TRY((Maps<3, R>::stencil(H, &f.tm_hi, f.halo_hi, 2)));
+  } else if (H->dims == 2) {
+    TRY((Maps<2, R>::stencil(H, &f.tm, f.ptr, H->nz)));
+    if (f.halo_lo) TRY((Maps<2, R>::stencil(H, &f.tm_lo, f.halo_lo, 2)));
+    if (f.halo_hi) TRY((Maps<2, R>::stencil(H, &f.tm_hi, f.halo_hi, 2)));
+  }
+  return NLSE2SHOC_OK;
+}
+
+static nlse2shoc_status encode_maps(nlse2shoc_t H, Field &f) {
+  return H->dtype == NLSE2SHOC_C64 ? encode_field_maps<float>(H, f) : encode_field_maps<double>(H, f);
+}
+
+template <typename R> static void build_tables(nlse2shoc_t H, std::vector<unsigned char> &host) {
+  // per-axis harmonic tables w_d (x_d - c_d)^2, x_d = xmin_d + i h_d, evaluated in double
+  const int ax_x = 0, ax_y = 1, ax_z = H->dims - 1;
+  std::vector<R> t;
+  auto add = [&](int ax, int64_t n) {
+    size_t off = t.size();
+    for (int64_t i = 0; i < n; ++i) {
+      const double x = H->V.xmin[ax] + double(i) * H->h[ax] - H->V.c[ax];
+      t.push_back(R(H->V.w[ax] * (x * x)));
+    }
+    while (t.size() % 4) t.push_back(R(0));
+    return off;
+  };
+  H->vx_off = add(ax_x, H->N[0]);
+  H->vy_off = H->dims == 3 ? add(ax_y, H->N[1]) : 0;
+  H->vz_off = H->dims >= 2 ? add(ax_z, H->N[ax_z]) : 0;
+  host.resize(t.size() * sizeof(R));
+  std::memcpy(host.data(), t.data(), host.size());
+}
+
+static nlse2shoc_status create_impl(nlse2shoc_t *out, int dims, const int64_t N[3], const double h[3], double a,
+                                    double s, const nlse2shoc_potential *V, nlse2shoc_bc bc, nlse2shoc_dtype dtype,
+                                    int rank, int nranks, const void *id128) {
+  if (!out) return fail(NLSE2SHOC_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (dims < 1 || dims > 3) return fail(NLSE2SHOC_EINVAL, "dims must be 1, 2 or 3");
+  if (!N || !h) return fail(NLSE2SHOC_EINVAL, "N / h is NULL");
+  for (int d = 0; d < 3; ++d) {
+    if (d < dims) {
+      if (N[d] < 5) return fail(NLSE2SHOC_EINVAL, "N[d] must be >= 5");
+      if (N[d] > (int64_t(1) << 31) - 64) return fail(NLSE2SHOC_EINVAL, "N[d] too large");
+      if (!finite_pos(h[d])) return fail(NLSE2SHOC_EINVAL, "h[d] must be finite and > 0");
+    } else if (N[d] != 1) {
+      return fail(NLSE2SHOC_EINVAL, "N[d] must be 1 for unused axes");
+    }
+  }
+  if (!finite_pos(a)) return fail(NLSE2SHOC_EINVAL, "a must be finite and > 0");
+  if (!std::isfinite(s)) return fail(NLSE2SHOC_EINVAL, "s must be finite");
+  if (bc != NLSE2SHOC_BC_DIRICHLET && bc != NLSE2SHOC_BC_LAPZERO) return fail(NLSE2SHOC_EINVAL, "bad bc");
+  if (dtype != NLSE2SHOC_C64 && dtype != NLSE2SHOC_C128) return fail(NLSE2SHOC_EINVAL, "bad dtype");
+  nlse2shoc_potential pv{};
+  pv.kind = NLSE2SHOC_V_NONE;
+  if (V) pv = *V;
+  if (pv.kind != NLSE2SHOC_V_NONE && pv.kind != NLSE2SHOC_V_HARMONIC && pv.kind != NLSE2SHOC_V_ARRAY)
+    return fail(NLSE2SHOC_EINVAL, "bad potential kind");
+  if (pv.kind == NLSE2SHOC_V_ARRAY && !pv.data) return fail(NLSE2SHOC_EINVAL, "V.data is NULL");
+  if (pv.kind == NLSE2SHOC_V_HARMONIC)
+    for (int d = 0; d < dims; ++d)
+      if (!std::isfinite(pv.w[d]) || !std::isfinite(pv.c[d]) || !std::isfinite(pv.xmin[d]))
+        return fail(NLSE2SHOC_EINVAL, "non-finite harmonic parameters");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(NLSE2SHOC_EINVAL, "bad rank / nranks");
+  if (nranks > 1 && dims == 1) return fail(NLSE2SHOC_EINVAL, "1D grids are not sharded (replicas only)");
+#ifndef NLSE_WITH_NCCL
+  if (nranks > 1) return fail(NLSE2SHOC_EUNSUPPORTED, "built without NCCL");
+#endif
+
+  auto *H = new nlse2shoc_s();
+  H->dims = dims;
+  for (int d = 0; d < 3; ++d) { H->N[d] = N[d]; H->h[d] = d < dims ? h[d] : 1.0; }
+  H->a = a;
+  H->s = s;
+  H->V = pv;
+  H->bc = bc;
+  H->dtype = dtype;
+  H->S = dtype == NLSE2SHOC_C64 ? 8 : 16;
+  H->rank = rank;
+  H->nranks = nranks;
+  H->sharded = id128 != nullptr;
+  cudaGetDevice(&H->device);
+  cudaDeviceGetAttribute(&H->num_sms, cudaDevAttrMultiProcessorCount, H->device);
+  H->NZ = dims >= 2 ? N[dims - 1] : 1;
+  H->nx = N[0];
+  H->ny = dims == 3 ? N[1] : 1;
+  int64_t z0 = 0, nz = H->NZ;
+  if (dims >= 2) nlse2shoc_split(H->NZ, nranks, rank, &z0, &nz);
+  if (dims >= 2 && nz < 2) { delete H; return fail(NLSE2SHOC_EINVAL, "each slab needs >= 2 planes"); }
+  H->z0 = z0;
+  H->nz = dims >= 2 ? nz : 1;
+  if (dims == 1) H->nz = 1;
+  const int64_t cpv = 16 / int64_t(H->S);
+  H->pitch = dims == 1 ? H->nx : ((H->nx + cpv - 1) / cpv) * cpv;
+  H->plane = H->pitch * H->ny;
+  H->local_elems = H->plane * H->nz;
+  *out = H;  // from here on, destroy() cleans up on failure
+
+  nlse2shoc_status st = NLSE2SHOC_OK;
+  auto chk = [&](nlse2shoc_status r) { if (st == NLSE2SHOC_OK) st = r; };
+  chk(alloc_field(H, H->TA, true));
+  chk(alloc_field(H, H->TB, true));
+  chk(alloc_field(H, H->acc, false));
+  if (st == NLSE2SHOC_OK && H->pitch != H->nx) chk(alloc_field(H, H->psiw, true));
+  if (st == NLSE2SHOC_OK && H->sharded && H->pitch == H->nx) {
+    // halo buffers for the caller's Psi (zero-copy path)
+    const size_t hb = size_t(2 * H->plane) * H->S;
+    if (cudaMalloc(&H->psiw.halo_lo, hb) != cudaSuccess || cudaMalloc(&H->psiw.halo_hi, hb) != cudaSuccess)
+      chk(fail(NLSE2SHOC_ENOMEM, "halo allocation failed"));
+    H->bytes += 2 * hb;
+  }
+  if (st == NLSE2SHOC_OK) {
+    chk(encode_maps(H, H->TA));
+    chk(encode_maps(H, H->TB));
+    if (H->psiw.ptr) chk(encode_maps(H, H->psiw));
+  }
+  if (st == NLSE2SHOC_OK && pv.kind == NLSE2SHOC_V_HARMONIC) {
+    std::vector<unsigned char> host;
+    if (dtype == NLSE2SHOC_C64) build_tables<float>(H, host);
+    else build_tables<double>(H, host);
+    if (cudaMalloc(&H->vtab, host.size()) != cudaSuccess) chk(fail(NLSE2SHOC_ENOMEM, "table allocation failed"));
+    else if (cudaMemcpy(H->vtab, host.data(), host.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+      chk(fail(NLSE2SHOC_ECUDA, "table upload failed"));
+    H->bytes += host.size();
+  }
+  if (st == NLSE2SHOC_OK) {
+    H->red_blocks = H->num_sms * 4;
+    if (cudaMalloc(&H->red, sizeof(double) * 3 * H->red_blocks) != cudaSuccess)
+      chk(fail(NLSE2SHOC_ENOMEM, "reduction buffer allocation failed"));
+  }
+#ifdef NLSE_WITH_NCCL
+  if (st == NLSE2SHOC_OK && H->sharded) {
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&H->comm, nranks, id, rank);
+    if (r != ncclSuccess) chk(fail(NLSE2SHOC_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r)));
+  }
+#endif
+  if (st == NLSE2SHOC_OK) {
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) chk(fail(NLSE2SHOC_ECUDA, cudaGetErrorString(e)));
+  }
+  if (st != NLSE2SHOC_OK) {
+    std::string keep = g_last_error;
+    nlse2shoc_destroy(H);
+    *out = nullptr;
+    g_last_error = keep;
+  }
+  return st;
+}
+
+// --------------------------------------------------------------------------- psi views
+// Wrap the caller's psi as the working Field (zero-copy) or stage it through the pitched
+// copy (only complex64 with odd N_x in 2D/3D, where rows are not 16-byte multiples).
+static nlse2shoc_status psi_in(nlse2shoc_t H, void *psi, Field &w, cudaStream_t st) {
+  if (H->pitch == H->nx) {
+    w.ptr = psi;
+    w.halo_lo = H->psiw.halo_lo;
+    w.halo_hi = H->psiw.halo_hi;
+    if (H->dims >= 2) {
+      if (H->dtype == NLSE2SHOC_C64) {
+        TRY(encode_field_maps<float>(H, w));
+      } else {
+        TRY(encode_field_maps<double>(H, w));
+      }
+    }
+    return NLSE2SHOC_OK;
+  }
+  w = H->psiw;
+  CUDA_TRY(cudaMemcpy2DAsync(w.ptr, H->pitch * H->S, psi, H->nx * H->S, H->nx * H->S, H->ny * H->nz,
+                             cudaMemcpyDeviceToDevice, st));
+  return NLSE2SHOC_OK;
+}
+
+static nlse2shoc_status psi_out(nlse2shoc_t H, void *psi, const void *src, cudaStream_t st) {
+  if (src == psi) return NLSE2SHOC_OK;
+  CUDA_TRY(cudaMemcpy2DAsync(psi, H->nx * H->S, src, H->pitch * H->S, H->nx * H->S, H->ny * H->nz,
+                             cudaMemcpyDeviceToDevice, st));
+  return NLSE2SHOC_OK;
+}
+
+static nlse2shoc_status check_ptr(const void *p, const char *name) {
+  if (!p) return fail(NLSE2SHOC_EINVAL, std::string(name) + " is NULL");
+  if (reinterpret_cast<uintptr_t>(p) % 16) return fail(NLSE2SHOC_EINVAL, std::string(name) + " is not 16-byte aligned");
+  return NLSE2SHOC_OK;
+}
+
+static nlse2shoc_status ensure_D(nlse2shoc_t H) {
+  if (H->D.ptr) return NLSE2SHOC_OK;
+  // D on local planes [-1, nz] (seam planes are recomputed from the Psi halo)
+  const size_t bytes = size_t(H->plane) * size_t(H->dims >= 2 ? H->nz + 2 : 1) * H->S;
+  CUDA_TRY(cudaMalloc(&H->D.ptr, bytes));
+  H->bytes += bytes;
+  return NLSE2SHOC_OK;
+}
+
+template <typename R> static nlse2shoc_status reduce_N(nlse2shoc_t H, const void *psi, double out[3], cudaStream_t st) {
+  StageParams<R> P;
+  fill_params<R>(H, P);
+  P.pitch = H->nx;  // caller layout
+  const int64_t total = H->nx * H->ny * H->nz;
+  const int blocks = int(std::min<int64_t>(H->red_blocks, (total + 255) / 256));
+  reduce_N_kernel<R><<<blocks, 256, 0, st>>>(reinterpret_cast<const cplx<R> *>(psi), P, H->red);
+  CUDA_TRY(cudaGetLastError());
+  std::vector<double> part(3 * blocks);
+  CUDA_TRY(cudaMemcpyAsync(part.data(), H->red, sizeof(double) * 3 * blocks, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  out[0] = INFINITY;
+  out[1] = -INFINITY;
+  out[2] = 0;
+  for (int b = 0; b < blocks; ++b) {
+    out[0] = std::min(out[0], part[3 * b]);
+    out[1] = std::max(out[1], part[3 * b + 1]);
+    out[2] += part[3 * b + 2];
+  }
+#ifdef NLSE_WITH_NCCL
+  if (H->sharded && H->nranks > 1) {
+    double *d = H->red;  // reuse: [-min, max, bad]
+    double v[3] = {-out[0], out[1], out[2]};
+    CUDA_TRY(cudaMemcpyAsync(d, v, sizeof(v), cudaMemcpyHostToDevice, st));
+    NCCL_TRY(ncclAllReduce(d, d, 2, ncclFloat64, ncclMax, H->comm, st));
+    NCCL_TRY(ncclAllReduce(d + 2, d + 2, 1, ncclFloat64, ncclSum, H->comm, st));
+    CUDA_TRY(cudaMemcpyAsync(v, d, sizeof(v), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    out[0] = -v[0];
+    out[1] = v[1];
+    out[2] = v[2];
+  }
+#endif
+  return NLSE2SHOC_OK;
+}
+
+// ===================================================================================== ABI
+extern "C" {
+
+nlse2shoc_status nlse2shoc_split(int64_t n_slow, int nranks, int rank, int64_t *z0, int64_t *nz) {
+  if (!z0 || !nz || nranks < 1 || rank < 0 || rank >= nranks || n_slow < 1) return fail(NLSE2SHOC_EINVAL, "bad split");
+  const int64_t base = n_slow / nranks, rem = n_slow % nranks;
+  *nz = base + (rank < rem ? 1 : 0);
+  *z0 = int64_t(rank) * base + std::min<int64_t>(rank, rem);
+  return NLSE2SHOC_OK;
+}
+
+nlse2shoc_status nlse2shoc_create(nlse2shoc_t *out, int dims, const int64_t N[3], const double h[3], double a, double s,
+                                  const nlse2shoc_potential *V, nlse2shoc_bc bc, nlse2shoc_dtype dtype) {
+  return create_impl(out, dims, N, h, a, s, V, bc, dtype, 0, 1, nullptr);
+}
+
+nlse2shoc_status nlse2shoc_get_unique_id(void *id128) {
+  if (!id128) return fail(NLSE2SHOC_EINVAL, "id128 is NULL");
+#ifdef NLSE_WITH_NCCL
+  ncclUniqueId id;
+  NCCL_TRY(ncclGetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "nccl unique id size");
+  std::memcpy(id128, &id, sizeof(id));
+  return NLSE2SHOC_OK;
+#else
+  return fail(NLSE2SHOC_EUNSUPPORTED, "built without NCCL");
+#endif
+}
+
+nlse2shoc_status nlse2shoc_create_sharded(nlse2shoc_t *out, int dims, const int64_t N[3], const double h[3], double a,
+                                          double s, const nlse2shoc_potential *V, nlse2shoc_bc bc,
+                                          nlse2shoc_dtype dtype, const void *id128, int rank, int nranks) {
+  if (!id128) return fail(NLSE2SHOC_EINVAL, "id128 is NULL");
+  return create_impl(out, dims, N, h, a, s, V, bc, dtype, rank, nranks, id128);
+}
+
+nlse2shoc_status nlse2shoc_local_extent(nlse2shoc_t H, int64_t *z0, int64_t *nz) {
+  if (!H || !z0 || !nz) return fail(NLSE2SHOC_EINVAL, "NULL argument");
+  *z0 = H->dims >= 2 ? H->z0 : 0;
+  *nz = H->dims >= 2 ? H->nz : H->N[0];
+  return NLSE2SHOC_OK;
+}
+
+size_t nlse2shoc_workspace_bytes(nlse2shoc_t H) { return H ? H->bytes : 0; }
+
+nlse2shoc_status nlse2shoc_set_variant(nlse2shoc_t H, int variant) {
+  if (!H) return fail(NLSE2SHOC_EINVAL, "NULL handle");
+  if (variant != 0 && variant != 1) return fail(NLSE2SHOC_EINVAL, "variant must be 0 (fused) or 1 (two-kernel)");
+  if (variant == 1) TRY(ensure_D(H));
+  H->variant = variant;
+  return NLSE2SHOC_OK;
+}
+
+nlse2shoc_status nlse2shoc_laplacian(nlse2shoc_t H, const void *psi, void *L, void *stream) {
+  if (!H) return fail(NLSE2SHOC_EINVAL, "NULL handle");
+  TRY(check_ptr(psi, "psi"));
+  TRY(check_ptr(L, "L"));
+  if (psi == L) return fail(NLSE2SHOC_EINVAL, "psi and L must be distinct");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  H->launches = 0;
+  Field w;
+  TRY(psi_in(H, const_cast<void *>(psi), w, st));
+  void *dst = H->pitch == H->nx ? L : H->TA.ptr;
+  const bool f64 = H->dtype == NLSE2SHOC_C64;
+  if (H->variant == 0) {
+    switch (H->dims) {
+      case 1: TRY(f64 ? (lap_fused<1, float>(H, w, dst, st)) : (lap_fused<1, double>(H, w, dst, st))); break;
+      case 2: TRY(f64 ? (lap_fused<2, float>(H, w, dst, st)) : (lap_fused<2, double>(H, w, dst, st))); break;
+      default: TRY(f64 ? (lap_fused<3, float>(H, w, dst, st)) : (lap_fused<3, double>(H, w, dst, st))); break;
+    }
+  } else {
+    switch (H->dims) {
+      case 1: TRY(f64 ? (lap_two<1, float>(H, w, dst, st)) : (lap_two<1, double>(H, w, dst, st))); break;
+      case 2: TRY(f64 ? (lap_two<2, float>(H, w, dst, st)) : (lap_two<2, double>(H, w, dst, st))); break;
+      default: TRY(f64 ? (lap_two<3, float>(H, w, dst, st)) : (lap_two<3, double>(H, w, dst, st))); break;
+    }
+  }
+  if (dst != L) TRY(psi_out(H, L, dst, st));
+  return NLSE2SHOC_OK;
+}
+
+nlse2shoc_status nlse2shoc_rk4(nlse2shoc_t H, void *psi, double dt, int64_t nsteps, void *stream) {
+  if (!H) return fail(NLSE2SHOC_EINVAL, "NULL handle");
+  TRY(check_ptr(psi, "psi"));
+  if (!finite_pos(dt)) return fail(NLSE2SHOC_EINVAL, "dt must be finite and > 0");
+  if (nsteps < 0) return fail(NLSE2SHOC_EINVAL, "nsteps must be >= 0");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  H->launches = 0;
+  if (nsteps == 0) return NLSE2SHOC_OK;
+  Field w;
+  TRY(psi_in(H, psi, w, st));
+  const bool f64 = H->dtype == NLSE2SHOC_C64;
+  if (H->variant == 0) {
+    switch (H->dims) {
+      case 1: TRY(f64 ? (rk4_fused<1, float>(H, w, dt, nsteps, st)) : (rk4_fused<1, double>(H, w, dt, nsteps, st))); break;
+      case 2: TRY(f64 ? (rk4_fused<2, float>(H, w, dt, nsteps, st)) : (rk4_fused<2, double>(H, w, dt, nsteps, st))); break;
+      default: TRY(f64 ? (rk4_fused<3, float>(H, w, dt, nsteps, st)) : (rk4_fused<3, double>(H, w, dt, nsteps, st))); break;
+    }
+  } else {
+    switch (H->dims) {
+      case 1: TRY(f64 ? (rk4_two<1, float>(H, w, dt, nsteps, st)) : (rk4_two<1, double>(H, w, dt, nsteps, st))); break;
+      case 2: TRY(f64 ? (rk4_two<2, float>(H, w, dt, nsteps, st)) : (rk4_two<2, double>(H, w, dt, nsteps, st))); break;
+      default: TRY(f64 ? (rk4_two<3, float>(H, w, dt, nsteps, st)) : (rk4_two<3, double>(H, w, dt, nsteps, st))); break;
+    }
+  }
+  return psi_out(H, psi, w.ptr, st);
+}
+
+nlse2shoc_status nlse2shoc_stability_bound(nlse2shoc_t H, const void *psi, double *kmax, void *stream) {
+  if (!H || !kmax) return fail(NLSE2SHOC_EINVAL, "NULL argument");
+  TRY(check_ptr(psi, "psi"));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  double r[3];
+  if (H->dtype == NLSE2SHOC_C64) TRY(reduce_N<float>(H, psi, r, st));
+  else TRY(reduce_N<double>(H, psi, r, st));
+  // `kdfull`: k < sqrt(8) / max(||B||, max_{i,g} |L_i - g|) h^2/a with B = 0 and
+  // G (Table 2) spanning [-4d/12, 64d/12] (Gershgorin endpoints of -h^2 Lap).  Written for a
+  // per-axis sum so that anisotropic h reduces to it (reading R17): with H = sum_d 1/h_d^2 the
+  // spectrum of (a Lap + N) lies in [Nmin - (64/12) a H, Nmax + (4/12) a H].
+  double Hs = 0.0;
+  for (int d = 0; d < H->dims; ++d) Hs += 1.0 / (H->h[d] * H->h[d]);
+  const double m1 = std::fabs((64.0 / 12.0) * H->a * Hs - r[0]);
+  const double m2 = std::fabs(r[1] + (4.0 / 12.0) * H->a * Hs);
+  *kmax = std::sqrt(8.0) / std::max(m1, m2);
+  if (r[2] > 0) return fail(NLSE2SHOC_ENONFINITE, "psi contains non-finite values");
+  return NLSE2SHOC_OK;
+}
+
+nlse2shoc_status nlse2shoc_check_finite(nlse2shoc_t H, const void *psi, void *stream) {
+  if (!H) return fail(NLSE2SHOC_EINVAL, "NULL handle");
+  TRY(check_ptr(psi, "psi"));
+  double r[3];
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (H->dtype == NLSE2SHOC_C64) TRY(reduce_N<float>(H, psi, r, st));
+  else TRY(reduce_N<double>(H, psi, r, st));
+  if (r[2] > 0) return fail(NLSE2SHOC_ENONFINITE, std::to_string(int64_t(r[2])) + " non-finite values");
+  return NLSE2SHOC_OK;
+}
+
+int64_t nlse2shoc_last_launch_count(nlse2shoc_t H) { return H ? H->launches : -1; }
+
+const char *nlse2shoc_strerror(nlse2shoc_status st) {
+  const int i = -int(st);
+  if (i < 0 || i > 6) return "unknown status";
+  return kErr[i];
+}
+
+const char *nlse2shoc_last_error(void) { return g_last_error.c_str(); }
+
+const char *nlse2shoc_version(void) {
+#ifdef NLSE_WITH_NCCL
+  return "nlse2shoc 0.1 sm_100a nccl";
+#else
+  return "nlse2shoc 0.1 sm_100a";
+#endif
+}
+
+void nlse2shoc_destroy(nlse2shoc_t H) {
+  if (!H) return;
+  cudaDeviceSynchronize();
+  for (Field *f : {&H->TA, &H->TB, &H->acc, &H->psiw, &H->D}) {
+    if (f->ptr) cudaFree(f->ptr);
+    if (f->halo_lo) cudaFree(f->halo_lo);
+    if (f->halo_hi) cudaFree(f->halo_hi);
+  }
+  if (H->vtab) cudaFree(H->vtab);
+  if (H->red) cudaFree(H->red);
+#ifdef NLSE_WITH_NCCL
+  if (H->comm) ncclCommDestroy(H->comm);
+#endif
+  delete H;
+}
+
+}  // extern "C"

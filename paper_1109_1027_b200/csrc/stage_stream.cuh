@@ -1,0 +1,440 @@
+// stage_stream.cuh — fused RK4-stage kernel for 2D / 3D grids on sm_100a.
+//
+// One launch = one RK4 stage s of one step over the whole (local) grid:
+//   * both 2SHOC steps (PAPER.md `2shoc1d`/`2shoc1d2` per axis; `3d2shocMs1/2`,
+//     P:263-276) folded into the algebraically equal 5-point-per-axis wide stencil
+//     (P:135-138), so the intermediate D never exists in memory;
+//   * the boundary rule for D (R8/R9) realised as ONE ghost value per face point,
+//     ghost = h_d^2 D_d(b) + 2 Psi_b - Psi_{b+n}, D_d(b) = lambda_b - sum_{e!=d} delta_e^2 Psi_b,
+//     computed in shared memory by the CTA that needs it (no extra pass, no padded arrays);
+//   * F = i(a Lap + (s|Psi|^2 - V) Psi) with the Psi_t boundary rule;
+//   * the RK4 stage combine in Psi-space accumulator form (16 field
+//     transfers per point-step instead of the listing's 17).
+//
+// Data movement: the slowest axis ("z"; y in 2D) is streamed.  A producer warp issues TMA
+// boxes of one plane (tile + 2-cell halo) into a ring of shared-memory slots guarded by
+// mbarriers, and the Psi^n / acc tiles the stage needs into a second ring; 8 consumer warps
+// compute plane k from slots k-2..k+2 and store T_s / acc with 128-bit stores.  Work is
+// split into (column, z-chunk) tiles assigned round-robin to a persistent grid so that
+// concurrently running CTAs work on neighbouring columns at the same z (halo re-reads hit
+// L2).  Shard seams (multi-GPU z-slabs) read their two halo planes through extra tensor
+// maps pointing at the halo buffers the NCCL exchange filled.
+#pragma once
+#include "common.cuh"
+
+namespace nlse {
+
+enum Mode { M_S1 = 1, M_S2 = 2, M_S3 = 3, M_S4 = 4, M_LAP = 5 };
+
+// Tile configuration per (dims, precision).  W = smem row width in complex elements
+// (tile + 2+2 halo, rounded so that it splits into NBOX equal TMA boxes); every TMA
+// destination must be 128-byte aligned, so box and slot byte sizes are multiples of 128,
+// and a box's inner extent must stay <= 256 eight-byte elements.
+template <int DIMS, typename R> struct Cfg;
+template <> struct Cfg<3, float> {
+  static constexpr int TX = 64, TY = 16, PPX = 2, RPW = 2, NCW = 8, RT = 8, RP = 4, NBOX = 1, NBOXP = 1, W = 68;
+};
+template <> struct Cfg<3, double> {
+  static constexpr int TX = 32, TY = 16, PPX = 1, RPW = 2, NCW = 8, RT = 8, RP = 4, NBOX = 1, NBOXP = 1, W = 36;
+};
+template <> struct Cfg<2, float> {
+  static constexpr int TX = 512, TY = 1, PPX = 2, RPW = 1, NCW = 8, RT = 12, RP = 6, NBOX = 3, NBOXP = 2, W = 528;
+};
+template <> struct Cfg<2, double> {
+  static constexpr int TX = 256, TY = 1, PPX = 1, RPW = 1, NCW = 8, RT = 12, RP = 6, NBOX = 3, NBOXP = 2, W = 264;
+};
+
+template <typename R> struct StageParams {
+  int nx, ny, nz;        // local extents: x, y (1 in 2D), streamed axis (local slab)
+  int z0, NZ;            // slab offset and global count of the streamed axis
+  int lo_face, hi_face;  // streamed-axis ends are global faces (1) or shard seams (0)
+  int has_lo_halo, has_hi_halo;
+  int ncx, ncy, nchunk;  // tile grid: columns in x, in y, z-chunks
+  int ntiles;
+  int64_t pitch;         // elements per x-row (all buffers)
+  int64_t plane;         // elements per plane = pitch * ny
+  R cx, cy, cz;          // 1/(12 h^2) per axis (wide-stencil scale)
+  R ihx2, ihy2, ihz2;    // 1/h^2 per axis (delta^2 in the face rule)
+  R hx2, hy2, hz2;       // h^2 per axis (ghost formula)
+  R a, s, inv_a;
+  R ca, cb;              // stage-combine coefficients (acc, T)
+  int bc;                // 0 Dirichlet, 1 Laplacian-zero
+  int vkind;             // 0 none, 1 harmonic tables, 2 array
+  const R *vx, *vy, *vz; // harmonic tables (vz indexed by GLOBAL streamed index)
+  const R *varr;         // array potential (local slab, row pitch nx)
+  cplx<R> *out_T;        // T_s (stages 1-3), psi^{n+1} (stage 4), L (laplacian mode)
+  cplx<R> *out_acc;      // accumulator (stages 1-3)
+};
+
+template <int DIMS, typename R> struct Layout {
+  using C = Cfg<DIMS, R>;
+  static constexpr int HY = DIMS == 3 ? 2 : 0;
+  static constexpr int SROWS = C::TY + 2 * HY;
+  static constexpr int SLOT = C::W * SROWS;                // complex per T slot
+  static constexpr int PTILE = C::TX * C::TY;              // complex per Psi / acc tile
+  static constexpr int EPC = sizeof(cplx<R>) / 8;          // 8-byte TMA elements per complex
+  static constexpr int BW = C::W * EPC / C::NBOX;          // T box inner extent (8-byte elems)
+  static constexpr int BWP = C::TX * EPC / C::NBOXP;       // Psi/acc box inner extent
+  static constexpr uint32_t SLOT_BYTES = SLOT * sizeof(cplx<R>);
+  static constexpr uint32_t PTILE_BYTES = PTILE * sizeof(cplx<R>);
+  static constexpr int NTHREADS = (C::NCW + 1) * 32;
+  static_assert(BW <= 256 && (BW * 8) % 16 == 0, "T box");
+  static_assert(BWP <= 256 && (BWP * 8) % 16 == 0, "P box");
+  static_assert(C::W * EPC % C::NBOX == 0 && C::TX * EPC % C::NBOXP == 0, "box split");
+  static_assert(C::W >= C::TX + 4, "row width");
+  static_assert(C::NBOX == 1 || SROWS == 1, "multi-box rows only for single-row slots");
+  static_assert(SLOT_BYTES % 128 == 0 && PTILE_BYTES % 128 == 0, "TMA destinations 128-byte aligned");
+  static_assert(C::NBOX == 1 || (BW * 8) % 128 == 0, "T sub-boxes 128-byte aligned");
+  static_assert(C::NBOXP == 1 || (BWP * 8) % 128 == 0, "P sub-boxes 128-byte aligned");
+  static_assert((C::TX / C::PPX) * (C::TY / C::RPW) == C::NCW * 32, "thread map");
+  template <int MODE> __host__ __device__ static constexpr bool needs_psi() { return MODE == M_S2 || MODE == M_S3; }
+  template <int MODE> __host__ __device__ static constexpr bool needs_acc() { return MODE == M_S2 || MODE == M_S3 || MODE == M_S4; }
+  template <int MODE> __host__ __device__ static constexpr int pa_tiles() { return (needs_psi<MODE>() ? 1 : 0) + (needs_acc<MODE>() ? 1 : 0); }
+  template <int MODE> __host__ __device__ static constexpr size_t smem_bytes() {
+    return 128 + size_t(C::RT) * SLOT_BYTES + size_t(pa_tiles<MODE>() ? C::RP : 0) * 2 * PTILE_BYTES +
+           size_t(2 * C::RT + 2 * C::RP) * 8;
+  }
+};
+
+template <typename R> __device__ __forceinline__ R potential(const StageParams<R> &P, int gx, int gy, int lz) {
+  if (P.vkind == 1) {  // ((w0 (x-c0)^2) + w1 (y-c1)^2) + w2 (z-c2)^2, absent axes dropped
+    R v = P.vx[gx];
+    if (P.vy) v = v + P.vy[gy];
+    if (P.vz) v = v + P.vz[P.z0 + lz];
+    return v;
+  }
+  if (P.vkind == 2) return P.varr[(int64_t(lz) * P.ny + gy) * P.nx + gx];
+  return R(0);
+}
+
+// lambda_b: boundary value of the total Laplacian (Dirichlet `dbc_lap` P:402; Laplacian-zero 0)
+template <typename R> __device__ __forceinline__ cplx<R> lambda_b(const StageParams<R> &P, cplx<R> c, R V) {
+  if (P.bc != 0) return mk<R>(R(0), R(0));
+  R N = fma(P.s, norm2(c), -V);
+  return mk<R>(-(N * c.re) * P.inv_a, -(N * c.im) * P.inv_a);
+}
+
+template <typename R> __device__ __forceinline__ cplx<R> d2(cplx<R> m, cplx<R> c, cplx<R> p, R ih2) {
+  return ih2 * ((m + p) - R(2) * c);
+}
+
+// Shared-memory 128-bit helpers: CPV complex values per 16-byte vector.
+template <typename R> struct V16;
+template <> struct V16<float> {
+  using T = float4;
+  static constexpr int CPV = 2;
+  __device__ static void split(const T &v, cplx<float> *o) { o[0] = {v.x, v.y}; o[1] = {v.z, v.w}; }
+  __device__ static T join(const cplx<float> *o) { return make_float4(o[0].re, o[0].im, o[1].re, o[1].im); }
+};
+template <> struct V16<double> {
+  using T = double2;
+  static constexpr int CPV = 1;
+  __device__ static void split(const T &v, cplx<double> *o) { o[0] = {v.x, v.y}; }
+  __device__ static T join(const cplx<double> *o) { return make_double2(o[0].re, o[0].im); }
+};
+
+template <typename R, int N>
+__device__ __forceinline__ void lds_run(const cplx<R> *p, cplx<R> *out) {
+  using VV = V16<R>;
+  static_assert(N % VV::CPV == 0, "run");
+#pragma unroll
+  for (int v = 0; v < N / VV::CPV; ++v) {
+    typename VV::T t = reinterpret_cast<const typename VV::T *>(p)[v];
+    VV::split(t, out + v * VV::CPV);
+  }
+}
+
+template <int DIMS, typename R, int MODE>
+__global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
+    stage_stream_kernel(const __grid_constant__ CUtensorMap tm_T, const __grid_constant__ CUtensorMap tm_lo,
+                        const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_psi,
+                        const __grid_constant__ CUtensorMap tm_acc, const StageParams<R> P) {
+  using C = Cfg<DIMS, R>;
+  using LY = Layout<DIMS, R>;
+  using CT = cplx<R>;
+  constexpr int HY = LY::HY, W = C::W, TX = C::TX, TY = C::TY;
+  constexpr int NPA = LY::template pa_tiles<MODE>();
+  constexpr int RP = NPA ? C::RP : 0;
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  CT *ring = reinterpret_cast<CT *>(base);
+  CT *pring = reinterpret_cast<CT *>(base + size_t(C::RT) * LY::SLOT_BYTES);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(base + size_t(C::RT) * LY::SLOT_BYTES + size_t(RP) * 2 * LY::PTILE_BYTES);
+  uint64_t *fullT = bars, *emptyT = bars + C::RT, *fullP = bars + 2 * C::RT, *emptyP = bars + 2 * C::RT + C::RP;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::RT; ++i) {
+      mbar_init(&fullT[i], 1);
+      mbar_init(&emptyT[i], C::NCW);
+    }
+    for (int i = 0; i < RP; ++i) {
+      mbar_init(&fullP[i], 1);
+      mbar_init(&emptyP[i], C::NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const int G = gridDim.x;
+  const int chunk_len = (P.nz + P.nchunk - 1) / P.nchunk;
+  const int ncol = P.ncx * P.ncy;
+
+  if (warp == C::NCW) {
+    // ------------------------------------------------------------------ producer warp
+    if (lane == 0) {
+      prefetch_tmap(&tm_T);
+      if (P.has_lo_halo) prefetch_tmap(&tm_lo);
+      if (P.has_hi_halo) prefetch_tmap(&tm_hi);
+      if (NPA) {
+        if (LY::template needs_psi<MODE>()) prefetch_tmap(&tm_psi);
+        if (LY::template needs_acc<MODE>()) prefetch_tmap(&tm_acc);
+      }
+      uint32_t tcnt = 0, pcnt = 0;
+      for (int t = blockIdx.x; t < P.ntiles; t += G) {
+        const int chunk = t / ncol, col = t % ncol;
+        const int x0 = (col % P.ncx) * TX, y0 = (col / P.ncx) * TY;
+        const int kb = chunk * chunk_len, ke = min(P.nz, kb + chunk_len);
+        auto produceT = [&](int p) {
+          const uint32_t slot = tcnt % C::RT, par = (tcnt / C::RT) & 1;
+          mbar_wait(&emptyT[slot], par ^ 1);
+          const CUtensorMap *m = nullptr;
+          int pz = p;
+          if (p >= 0 && p < P.nz) m = &tm_T;
+          else if (p < 0 && P.has_lo_halo) { m = &tm_lo; pz = p + 2; }
+          else if (p >= P.nz && P.has_hi_halo) { m = &tm_hi; pz = p - P.nz; }
+          if (m) {
+            mbar_arrive_expect_tx(&fullT[slot], LY::SLOT_BYTES);
+            CT *dst = ring + size_t(slot) * LY::SLOT;
+#pragma unroll
+            for (int b = 0; b < C::NBOX; ++b) {
+              const int c0 = (x0 - 2) * LY::EPC + b * LY::BW;
+              if (DIMS == 3) tma_load_3d(reinterpret_cast<char *>(dst) + b * LY::BW * 8, m, &fullT[slot], c0, y0 - 2, pz);
+              else tma_load_2d(reinterpret_cast<char *>(dst) + b * LY::BW * 8, m, &fullT[slot], c0, pz);
+            }
+          } else {
+            mbar_arrive(&fullT[slot]);
+          }
+          ++tcnt;
+        };
+        auto produceP = [&](int k) {
+          const uint32_t slot = pcnt % C::RP, par = (pcnt / C::RP) & 1;
+          mbar_wait(&emptyP[slot], par ^ 1);
+          mbar_arrive_expect_tx(&fullP[slot], NPA * LY::PTILE_BYTES);
+          CT *dst = pring + size_t(slot) * 2 * LY::PTILE;
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const bool want = q == 0 ? LY::template needs_psi<MODE>() : LY::template needs_acc<MODE>();
+            if (!want) continue;
+            const CUtensorMap *m = q == 0 ? &tm_psi : &tm_acc;
+#pragma unroll
+            for (int b = 0; b < C::NBOXP; ++b) {
+              const int c0 = x0 * LY::EPC + b * LY::BWP;
+              char *d = reinterpret_cast<char *>(dst + q * LY::PTILE) + b * LY::BWP * 8;
+              if (DIMS == 3) tma_load_3d(d, m, &fullP[slot], c0, y0, k);
+              else tma_load_2d(d, m, &fullP[slot], c0, k);
+            }
+          }
+          ++pcnt;
+        };
+        for (int p = kb - 2; p < kb + 2; ++p) produceT(p);
+        for (int k = kb; k < ke; ++k) {
+          produceT(k + 2);
+          if (NPA) produceP(k);
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------------- consumer warps
+  const int ct = threadIdx.x;                      // 0 .. NCW*32-1
+  constexpr int CPT = TX / C::PPX;                 // column groups per row
+  const int cg = ct % CPT, rg = ct / CPT;
+  const int lx0 = cg * C::PPX;                     // first local x of this thread
+  const int ly0 = rg * C::RPW;                     // first local row of this thread
+  uint32_t tcnt = 0, pcnt = 0;
+
+  for (int t = blockIdx.x; t < P.ntiles; t += G) {
+    const int chunk = t / ncol, col = t % ncol;
+    const int x0 = (col % P.ncx) * TX, y0 = (col / P.ncx) * TY;
+    const int kb = chunk * chunk_len, ke = min(P.nz, kb + chunk_len);
+    const uint32_t tbase = tcnt;  // ring counter of plane kb-2
+    auto tslot = [&](int p) -> CT * { return ring + size_t((tbase + uint32_t(p - kb + 2)) % C::RT) * LY::SLOT; };
+    auto twait = [&](int p) {
+      const uint32_t c = tbase + uint32_t(p - kb + 2);
+      mbar_wait(&fullT[c % C::RT], (c / C::RT) & 1);
+    };
+    auto trelease = [&](int p) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&emptyT[(tbase + uint32_t(p - kb + 2)) % C::RT]);
+    };
+    for (int p = kb - 2; p < kb + 2; ++p) twait(p);
+
+    // tile facts (CTA-uniform)
+    const bool xlo = x0 == 0, xhi = (x0 <= P.nx - 2) && (P.nx - 2 < x0 + TX);
+    const bool ylo = DIMS == 3 && y0 == 0, yhi = DIMS == 3 && (y0 <= P.ny - 2) && (P.ny - 2 < y0 + TY);
+
+    for (int k = kb; k < ke; ++k) {
+      twait(k + 2);
+      CT *pa = nullptr;
+      if (NPA) {
+        const uint32_t slot = pcnt % C::RP;
+        mbar_wait(&fullP[slot], (pcnt / C::RP) & 1);
+        pa = pring + size_t(slot) * 2 * LY::PTILE;
+      }
+      const int gz = P.z0 + k;  // global streamed index
+      const bool zint = gz >= 1 && gz <= P.NZ - 2;
+      const bool zg_lo = P.lo_face && k == 1;
+      const bool zg_hi = P.hi_face && k == P.nz - 2;
+      const bool do_ghost = (zint && (xlo || xhi || ylo || yhi)) || zg_lo || zg_hi;
+
+      if (do_ghost) {
+        // ---- ghost values (reading R8/R9, ghost form): one per face point that a depth-1
+        // interior point of this tile/plane reads.
+        CT *s0 = tslot(k), *sm = tslot(k - 1), *sp = tslot(k + 1);
+        auto at = [&](CT *s, int lx, int ly) -> CT & { return s[(ly + HY) * W + lx + 2]; };
+        if (zint) {
+          // x faces: rows of the tile (3D: interior rows only)
+          for (int task = ct; task < 2 * TY; task += C::NCW * 32) {
+            const bool hi = task >= TY;
+            if (hi ? !xhi : !xlo) continue;
+            const int ly = task % TY, gy = y0 + ly;
+            if (DIMS == 3 && (gy < 1 || gy > P.ny - 2)) continue;
+            if (gy >= P.ny) continue;
+            const int bx = hi ? P.nx - 1 : 0, lb = bx - x0, n = hi ? -1 : 1;
+            CT cb = at(s0, lb, ly), cin = at(s0, lb + n, ly);
+            CT D = lambda_b(P, cb, potential(P, bx, gy, k));
+            D = D - d2(at(sm, lb, ly), cb, at(sp, lb, ly), P.ihz2);
+            if (DIMS == 3) D = D - d2(at(s0, lb, ly - 1), cb, at(s0, lb, ly + 1), P.ihy2);
+            at(s0, lb - n, ly) = axpy(R(2) * cb - cin, P.hx2, D);
+          }
+          if (DIMS == 3) {
+            for (int task = ct; task < 2 * TX; task += C::NCW * 32) {
+              const bool hi = task >= TX;
+              if (hi ? !yhi : !ylo) continue;
+              const int lx = task % TX, gx = x0 + lx;
+              if (gx < 1 || gx > P.nx - 2) continue;
+              const int by = hi ? P.ny - 1 : 0, lb = by - y0, n = hi ? -1 : 1;
+              CT cb = at(s0, lx, lb), cin = at(s0, lx, lb + n);
+              CT D = lambda_b(P, cb, potential(P, gx, by, k));
+              D = D - d2(at(sm, lx, lb), cb, at(sp, lx, lb), P.ihz2);
+              D = D - d2(at(s0, lx - 1, lb), cb, at(s0, lx + 1, lb), P.ihx2);
+              at(s0, lx, lb - n) = axpy(R(2) * cb - cin, P.hy2, D);
+            }
+          }
+        }
+        if (zg_lo || zg_hi) {
+          // streamed-axis face: ghost plane -1 (before output plane 1) or nz (before nz-2)
+          const int bz = zg_lo ? 0 : P.nz - 1, n = zg_lo ? 1 : -1;
+          CT *sb = tslot(bz), *si = tslot(bz + n), *sg = tslot(bz - n);
+          for (int task = ct; task < TX * TY; task += C::NCW * 32) {
+            const int lx = task % TX, ly = task / TX, gx = x0 + lx, gy = y0 + ly;
+            if (gx < 1 || gx > P.nx - 2) continue;
+            if (DIMS == 3 && (gy < 1 || gy > P.ny - 2)) continue;
+            CT cb = at(sb, lx, ly), cin = at(si, lx, ly);
+            CT D = lambda_b(P, cb, potential(P, gx, gy, bz));
+            D = D - d2(at(sb, lx - 1, ly), cb, at(sb, lx + 1, ly), P.ihx2);
+            if (DIMS == 3) D = D - d2(at(sb, lx, ly - 1), cb, at(sb, lx, ly + 1), P.ihy2);
+            at(sg, lx, ly) = axpy(R(2) * cb - cin, P.hz2, D);
+          }
+        }
+        fence_proxy_async_smem();  // generic writes to slots precede later TMA refills
+        named_bar_sync(1, C::NCW * 32);
+      }
+
+      // ---- stencil + RHS + stage combine for this thread's points of plane k
+      const CT *s0 = tslot(k), *sm1 = tslot(k - 1), *sp1 = tslot(k + 1), *sm2 = tslot(k - 2), *sp2 = tslot(k + 2);
+#pragma unroll
+      for (int r = 0; r < C::RPW; ++r) {
+        const int ly = ly0 + r, gy = y0 + ly;
+        const int srow = (ly + HY) * W;
+        CT run[C::PPX + 4];
+        lds_run<R, C::PPX + 4>(s0 + srow + lx0, run);
+        CT zm2[C::PPX], zm1[C::PPX], zp1[C::PPX], zp2[C::PPX];
+        lds_run<R, C::PPX>(sm2 + srow + lx0 + 2, zm2);
+        lds_run<R, C::PPX>(sm1 + srow + lx0 + 2, zm1);
+        lds_run<R, C::PPX>(sp1 + srow + lx0 + 2, zp1);
+        lds_run<R, C::PPX>(sp2 + srow + lx0 + 2, zp2);
+        CT ym2[C::PPX], ym1[C::PPX], yp1[C::PPX], yp2[C::PPX];
+        if (DIMS == 3) {
+          lds_run<R, C::PPX>(s0 + srow - 2 * W + lx0 + 2, ym2);
+          lds_run<R, C::PPX>(s0 + srow - W + lx0 + 2, ym1);
+          lds_run<R, C::PPX>(s0 + srow + W + lx0 + 2, yp1);
+          lds_run<R, C::PPX>(s0 + srow + 2 * W + lx0 + 2, yp2);
+        }
+        CT psv[C::PPX], acv[C::PPX];
+        if (LY::template needs_psi<MODE>()) lds_run<R, C::PPX>(pa + ly * TX + lx0, psv);
+        if (LY::template needs_acc<MODE>()) lds_run<R, C::PPX>(pa + LY::PTILE + ly * TX + lx0, acv);
+
+        CT oT[C::PPX], oA[C::PPX];
+        bool valid[C::PPX];
+#pragma unroll
+        for (int q = 0; q < C::PPX; ++q) {
+          const int gx = x0 + lx0 + q;
+          valid[q] = gx < P.nx && gy < P.ny;
+          const CT c = run[q + 2];
+          const bool bnd = gx == 0 || gx == P.nx - 1 || (DIMS == 3 && (gy == 0 || gy == P.ny - 1)) || gz == 0 ||
+                           gz == P.NZ - 1;
+          const R V = valid[q] ? potential(P, gx, gy, k) : R(0);
+          const R N = fma(P.s, norm2(c), -V);
+          CT F, L;
+          if (!bnd) {
+            // 5-point wide form per axis, (-g2 + 16 g1 - 30 g0 + 16 g-1 - g-2)/(12 h^2)
+            L = P.cx * (R(16) * (run[q + 1] + run[q + 3]) - (run[q] + run[q + 4]) - R(30) * c);
+            L = L + P.cz * (R(16) * (zm1[q] + zp1[q]) - (zm2[q] + zp2[q]) - R(30) * c);
+            if (DIMS == 3) L = L + P.cy * (R(16) * (ym1[q] + yp1[q]) - (ym2[q] + yp2[q]) - R(30) * c);
+            // F = i (a L + N c)
+            F = mk<R>(-fma(P.a, L.im, N * c.im), fma(P.a, L.re, N * c.re));
+          } else {
+            L = lambda_b(P, c, V);
+            F = P.bc == 0 ? mk<R>(R(0), R(0)) : mk<R>(-(N * c.im), N * c.re);
+          }
+          if (MODE == M_LAP) {
+            oT[q] = L;
+          } else if (MODE == M_S1) {
+            oA[q] = axpy(c, P.ca, F);
+            oT[q] = axpy(c, P.cb, F);
+          } else if (MODE == M_S2 || MODE == M_S3) {
+            oA[q] = axpy(acv[q], P.ca, F);
+            oT[q] = axpy(psv[q], P.cb, F);
+          } else {  // M_S4
+            oT[q] = axpy(acv[q], P.cb, F);
+          }
+        }
+        // ---- stores (128-bit when all PPX points are inside the grid)
+        const int64_t gidx = int64_t(k) * P.plane + int64_t(gy) * P.pitch + (x0 + lx0);
+        using VV = V16<R>;
+        bool all = true;
+#pragma unroll
+        for (int q = 0; q < C::PPX; ++q) all = all && valid[q];
+        if (all) {
+#pragma unroll
+          for (int v = 0; v < C::PPX / VV::CPV; ++v) {
+            reinterpret_cast<typename VV::T *>(P.out_T + gidx)[v] = VV::join(oT + v * VV::CPV);
+            if (MODE != M_LAP && MODE != M_S4)
+              reinterpret_cast<typename VV::T *>(P.out_acc + gidx)[v] = VV::join(oA + v * VV::CPV);
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < C::PPX; ++q) {
+            if (!valid[q]) continue;
+            P.out_T[gidx + q] = oT[q];
+            if (MODE != M_LAP && MODE != M_S4) P.out_acc[gidx + q] = oA[q];
+          }
+        }
+      }
+      if (NPA) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&emptyP[pcnt % C::RP]);
+        ++pcnt;
+      }
+      trelease(k - 2);
+    }
+    for (int p = ke - 2; p < ke + 2; ++p) trelease(p);
+    tcnt = tbase + uint32_t(ke - kb + 4);
+  }
+}
+
+}  // namespace nlse

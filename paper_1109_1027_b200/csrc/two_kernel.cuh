@@ -1,0 +1,180 @@
+// two_kernel.cuh — the paper's own single-storage 2SHOC realisation ("TWO_KERNEL" variant),
+// kept beside the fused kernel as the paper-faithful comparison point.
+//
+// Kernel A (step 1, `2d2shocs1` P:205-214, `3d2shocs` P:286-308):
+//     D = sum_d delta_d^2 Psi at interior points, D_b = lambda_b at boundary points
+//     (`dbc_lap` P:399-404; Laplacian-zero P:431), stored to HBM (one extra field).
+// Kernel B (step 2 + RHS + RK4 stage combine):
+//   isotropic h, the paper's printed stencils (`2d2shocs2` P:218-232, `3d2shocs2`
+//   P:312-354; 1D `2shoc1d2` P:132):
+//     L = -1/12 (sum_{2d neighbours} D - (16 - 2d) D) + 1/(6h^2) (sum_{edge-midpoints} Psi - 4 p Psi),
+//     p = d(d-1)/2 coordinate planes;
+//   anisotropic h (reading R17): the same operator written per axis,
+//     L = D - sum_d (D(+e_d) + D(-e_d) - 2D)/12
+//           + sum_{d<e} (h_d^2 + h_e^2)/12 * delta_d^2 delta_e^2 Psi.
+// Shard seams: D is also evaluated on the two planes adjacent to the slab (from the 2-plane
+// Psi halo), so one halo exchange per stage serves both steps.
+#pragma once
+#include "stage_stream.cuh"
+
+namespace nlse {
+
+template <typename R> struct TwoParams {
+  int iso;
+  R w2;             // isotropic: 1/(6 h^2)
+  R cde[3];         // anisotropic pair weights (h_d^2 + h_e^2)/(12 h_d^2 h_e^2) for (x,y),(x,z),(y,z)
+};
+
+template <typename R> static void two_params(int dims, const double h[3], TwoParams<R> &Q) {
+  Q.iso = 1;
+  for (int d = 1; d < dims; ++d)
+    if (h[d] != h[0]) Q.iso = 0;
+  Q.w2 = R(1.0 / (6.0 * h[0] * h[0]));
+  // kernel axes: x = axis 0, y = axis 1 (3D), z = streamed axis (dims-1)
+  const double hx = h[0], hy = dims == 3 ? h[1] : 1.0, hz = dims >= 2 ? h[dims - 1] : 1.0;
+  auto c = [](double a, double b) { return (a * a + b * b) / (12.0 * a * a * b * b); };
+  Q.cde[0] = R(c(hx, hy));
+  Q.cde[1] = R(c(hx, hz));
+  Q.cde[2] = R(c(hy, hz));
+}
+
+template <typename R> struct PlaneView {  // stencil-input planes incl. the 2-plane halos
+  const cplx<R> *in, *lo, *hi;
+  int nz;
+  int64_t plane;
+  __device__ __forceinline__ const cplx<R> *operator()(int p) const {
+    if (p >= 0 && p < nz) return in + int64_t(p) * plane;
+    if (p < 0) return lo + int64_t(p + 2) * plane;
+    return hi + int64_t(p - nz) * plane;
+  }
+};
+
+// Kernel A: D on local planes [-1, nz] (index shifted by +1 in the D buffer).
+template <int DIMS, typename R>
+__global__ void __launch_bounds__(256) two_d_kernel(PlaneView<R> T, cplx<R> *__restrict__ D, const StageParams<R> P) {
+  // 3D blocks cover 32 x 8 points of a plane, 1D/2D blocks 256 points of a row
+  const int gx = DIMS == 3 ? blockIdx.x * 32 + (threadIdx.x & 31) : blockIdx.x * 256 + threadIdx.x;
+  const int gy = DIMS == 3 ? blockIdx.y * 8 + (threadIdx.x >> 5) : 0;
+  const int lz = DIMS >= 2 ? int(blockIdx.z) - 1 : 0;
+  if (gx >= P.nx || gy >= P.ny) return;
+  const int gz = P.z0 + lz;
+  if (DIMS >= 2 && (gz < 0 || gz >= P.NZ)) return;  // beyond a global face: never read
+  const cplx<R> *pl = T(DIMS >= 2 ? lz : 0);
+  const int64_t o = int64_t(gy) * P.pitch + gx;
+  const cplx<R> c = pl[o];
+  const bool bnd = gx == 0 || gx == P.nx - 1 || (DIMS == 3 && (gy == 0 || gy == P.ny - 1)) ||
+                   (DIMS >= 2 && (gz == 0 || gz == P.NZ - 1));
+  cplx<R> d;
+  if (bnd) {
+    d = lambda_b(P, c, potential(P, gx, gy, lz));
+  } else {
+    d = d2(pl[o - 1], c, pl[o + 1], P.ihx2);
+    if (DIMS == 3) d = d + d2(pl[o - P.pitch], c, pl[o + P.pitch], P.ihy2);
+    if (DIMS >= 2) d = d + d2(T(lz - 1)[o], c, T(lz + 1)[o], P.ihz2);
+  }
+  D[(int64_t(DIMS >= 2 ? lz + 1 : 0)) * P.plane + o] = d;
+}
+
+// Kernel B: step 2 + F + stage combine (MODE 1-4) or L (MODE 5) on local planes [0, nz).
+template <int DIMS, typename R, int MODE>
+__global__ void __launch_bounds__(256) two_step2_kernel(PlaneView<R> T, const cplx<R> *__restrict__ D,
+                                                         const cplx<R> *__restrict__ psi,
+                                                         const cplx<R> *__restrict__ acc, const StageParams<R> P,
+                                                         const TwoParams<R> Q) {
+  // 3D blocks cover 32 x 8 points of a plane, 1D/2D blocks 256 points of a row
+  const int gx = DIMS == 3 ? blockIdx.x * 32 + (threadIdx.x & 31) : blockIdx.x * 256 + threadIdx.x;
+  const int gy = DIMS == 3 ? blockIdx.y * 8 + (threadIdx.x >> 5) : 0;
+  const int lz = blockIdx.z;
+  if (gx >= P.nx || gy >= P.ny) return;
+  const int gz = P.z0 + lz;
+  const int64_t o = int64_t(gy) * P.pitch + gx;
+  const cplx<R> *pl = T(lz);
+  const cplx<R> c = pl[o];
+  const bool bnd = gx == 0 || gx == P.nx - 1 || (DIMS == 3 && (gy == 0 || gy == P.ny - 1)) ||
+                   (DIMS >= 2 && (gz == 0 || gz == P.NZ - 1));
+  const R V = potential(P, gx, gy, lz);
+  const R N = fma(P.s, norm2(c), -V);
+  cplx<R> L, F;
+  if (!bnd) {
+    const int64_t dz = DIMS >= 2 ? P.plane : 0;
+    const cplx<R> *Dc = D + (DIMS >= 2 ? int64_t(lz + 1) * P.plane : 0) + o;
+    const cplx<R> d0 = Dc[0];
+    cplx<R> sx = Dc[-1] + Dc[1];
+    cplx<R> sy = DIMS == 3 ? Dc[-P.pitch] + Dc[P.pitch] : mk<R>(R(0), R(0));
+    cplx<R> sz = DIMS >= 2 ? Dc[-dz] + Dc[dz] : mk<R>(R(0), R(0));
+    if (Q.iso) {
+      // -1/12 (sum of 2d D-neighbours - (16 - 2d) D) + 1/(6h^2) (edge-midpoints - 4 p Psi)
+      L = R(-1.0 / 12.0) * ((sx + sy + sz) - R(16 - 2 * DIMS) * d0);
+      if (DIMS >= 2) {
+        cplx<R> e = mk<R>(R(0), R(0));
+        const cplx<R> *zm = T(lz - 1) + o, *zp = T(lz + 1) + o;
+        if (DIMS == 3) {
+          e = e + (pl[o - P.pitch - 1] + pl[o - P.pitch + 1]) + (pl[o + P.pitch - 1] + pl[o + P.pitch + 1]);
+          e = e + (zm[-P.pitch] + zm[P.pitch]) + (zp[-P.pitch] + zp[P.pitch]);
+        }
+        e = e + (zm[-1] + zm[1]) + (zp[-1] + zp[1]);
+        const int npairs = DIMS * (DIMS - 1) / 2;
+        L = L + Q.w2 * (e - R(4 * npairs) * c);
+      }
+    } else {
+      L = d0 - R(1.0 / 12.0) * ((sx + sy + sz) - R(2 * DIMS) * d0);
+      // sum_{d<e} (h_d^2+h_e^2)/12 delta_d^2 delta_e^2 Psi, each cross difference written as
+      // [corners - 2 (face neighbours of both axes) + 4 Psi] / (h_d^2 h_e^2)
+      auto cross = [&](cplx<R> corners, cplx<R> fd, cplx<R> fe, R w) {
+        return w * ((corners - R(2) * (fd + fe)) + R(4) * c);
+      };
+      const cplx<R> fx = pl[o - 1] + pl[o + 1];
+      if (DIMS >= 2) {
+        const cplx<R> *zm = T(lz - 1) + o, *zp = T(lz + 1) + o;
+        const cplx<R> fz = zm[0] + zp[0];
+        L = L + cross((zm[-1] + zm[1]) + (zp[-1] + zp[1]), fx, fz, Q.cde[1]);
+        if (DIMS == 3) {
+          const cplx<R> fy = pl[o - P.pitch] + pl[o + P.pitch];
+          L = L + cross((pl[o - P.pitch - 1] + pl[o - P.pitch + 1]) + (pl[o + P.pitch - 1] + pl[o + P.pitch + 1]), fx,
+                        fy, Q.cde[0]);
+          L = L + cross((zm[-P.pitch] + zm[P.pitch]) + (zp[-P.pitch] + zp[P.pitch]), fy, fz, Q.cde[2]);
+        }
+      }
+    }
+    F = mk<R>(-fma(P.a, L.im, N * c.im), fma(P.a, L.re, N * c.re));
+  } else {
+    L = lambda_b(P, c, V);
+    F = P.bc == 0 ? mk<R>(R(0), R(0)) : mk<R>(-(N * c.im), N * c.re);
+  }
+  const int64_t g = int64_t(lz) * P.plane + o;
+  if (MODE == M_LAP) {
+    P.out_T[g] = L;
+  } else if (MODE == M_S1) {
+    P.out_acc[g] = axpy(c, P.ca, F);
+    P.out_T[g] = axpy(c, P.cb, F);
+  } else if (MODE == M_S2 || MODE == M_S3) {
+    P.out_acc[g] = axpy(acc[g], P.ca, F);
+    P.out_T[g] = axpy(psi[g], P.cb, F);
+  } else {
+    P.out_T[g] = axpy(acc[g], P.cb, F);
+  }
+}
+
+template <int DIMS, typename R>
+static cudaError_t launch_two_impl(int stage, const cplx<R> *in, const cplx<R> *lo, const cplx<R> *hi,
+                                   const cplx<R> *psi, const cplx<R> *acc, cplx<R> *D, const StageParams<R> &P,
+                                   const TwoParams<R> &Q, cudaStream_t st) {
+  PlaneView<R> T{in, lo ? lo : in, hi ? hi : in, P.nz, P.plane};
+  dim3 blk(256);
+  const int bx = DIMS == 3 ? (P.nx + 31) / 32 : (P.nx + 255) / 256;
+  dim3 ga(bx, DIMS == 3 ? (P.ny + 7) / 8 : 1, DIMS >= 2 ? P.nz + 2 : 1);
+  two_d_kernel<DIMS, R><<<ga, blk, 0, st>>>(T, D, P);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  dim3 gb(bx, DIMS == 3 ? (P.ny + 7) / 8 : 1, DIMS >= 2 ? P.nz : 1);
+  switch (stage) {
+    case 1: two_step2_kernel<DIMS, R, M_S1><<<gb, blk, 0, st>>>(T, D, psi, acc, P, Q); break;
+    case 2: two_step2_kernel<DIMS, R, M_S2><<<gb, blk, 0, st>>>(T, D, psi, acc, P, Q); break;
+    case 3: two_step2_kernel<DIMS, R, M_S3><<<gb, blk, 0, st>>>(T, D, psi, acc, P, Q); break;
+    case 4: two_step2_kernel<DIMS, R, M_S4><<<gb, blk, 0, st>>>(T, D, psi, acc, P, Q); break;
+    default: two_step2_kernel<DIMS, R, M_LAP><<<gb, blk, 0, st>>>(T, D, psi, acc, P, Q); break;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace nlse

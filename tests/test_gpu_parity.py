@@ -1,0 +1,235 @@
+"""GPU <-> oracle parity through the C-ABI (needs a B200).
+
+Tolerances (north star, written here): max relative L2 <= 1e-12 for complex128 and
+<= 1e-5 for complex64 after the stated steps; the oracle runs in double from the same
+(float-rounded for c64) seeded input (reading R19).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from icgen import configs
+
+import harness as H
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+SHAPES = {
+    1: [(5,), (7,), (37,), (1001,)],
+    2: [(5, 5), (7, 6), (37, 13), (530, 9), (1030, 7)],
+    3: [(5, 5, 5), (7, 6, 5), (37, 19, 9), (70, 35, 11), (130, 17, 7)],
+}
+
+
+def _small(dims, n, bc, dtype, V, aniso=True):
+    h = [0.11, 0.13, 0.17][:dims] if aniso else [0.12] * dims
+    return configs.SMALL(dims, n, bc, dtype=dtype, V=V, h=h)
+
+
+CASES = []
+for dims in (1, 2, 3):
+    for i, n in enumerate(SHAPES[dims]):
+        for dtype in ("c64", "c128"):
+            for bc in ("dirichlet", "lapzero"):
+                V = ["harmonic", "array", "none"][(i + (bc == "lapzero")) % 3]
+                CASES.append((dims, n, dtype, bc, V))
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("dims,n,dtype,bc,V", CASES)
+def test_laplacian_parity(dims, n, dtype, bc, V, variant):
+    w = _small(dims, n, bc, dtype, V, aniso=(variant == 0 or dims != 2))
+    S = H.gpu_solver(w, dtype, variant)
+    psi = H.psi0_host(w, dtype)
+    L = S.laplacian(_dev(psi))
+    torch.cuda.synchronize()
+    Lo = oracle.laplacian(H.oracle_problem(w), psi.astype(np.complex128))
+    tol = 1e-12 if dtype == "c128" else 1e-5
+    assert H.rel_l2(L.cpu().numpy(), Lo) <= tol
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("dims,n,dtype,bc,V", CASES[::2])
+def test_rk4_parity_10_steps(dims, n, dtype, bc, V, variant):
+    w = _small(dims, n, bc, dtype, V)
+    S = H.gpu_solver(w, dtype, variant)
+    psi = H.psi0_host(w, dtype)
+    P = H.oracle_problem(w)
+    dt = 0.8 * oracle.kmax(P, psi.astype(np.complex128))
+    g = _dev(psi)
+    S.rk4(g, dt, 10)
+    torch.cuda.synchronize()
+    ref = oracle.rk4(P, psi.astype(np.complex128), dt, 10)
+    assert H.rel_l2(g.cpu().numpy(), ref) <= H.TOL[dtype]
+
+
+@pytest.mark.parametrize("dims,n,dtype,bc,V", [c for c in CASES if c[2] == "c128"][::3])
+def test_stability_bound_matches_oracle(dims, n, dtype, bc, V):
+    w = _small(dims, n, bc, dtype, V)
+    S = H.gpu_solver(w, dtype)
+    psi = H.psi0_host(w, dtype)
+    k = S.stability_bound(_dev(psi))
+    ko = oracle.kmax(H.oracle_problem(w), psi)
+    assert abs(k - ko) <= 1e-13 * ko
+
+
+def test_fused_and_two_kernel_agree_3d():
+    w = _small(3, (70, 35, 11), "dirichlet", "c128", "harmonic", aniso=False)
+    psi = H.psi0_host(w, "c128")
+    outs = []
+    for v in (0, 1):
+        S = H.gpu_solver(w, "c128", v)
+        g = _dev(psi)
+        S.rk4(g, 1e-4, 5)
+        outs.append(g.cpu().numpy())
+    assert H.rel_l2(outs[0], outs[1]) <= 1e-13
+
+
+def test_edge_cases_and_errors():
+    import paper_1109_1027_b200 as nl
+
+    w = _small(3, (9, 8, 7), "dirichlet", "c64", "harmonic")
+    S = H.gpu_solver(w, "c64")
+    psi = _dev(H.psi0_host(w, "c64"))
+    before = psi.clone()
+    S.rk4(psi, 1e-3, 0)  # nsteps = 0 is a no-op
+    assert torch.equal(psi, before)
+    with pytest.raises(nl.NLSE2SHOCError):
+        S.rk4(psi, -1.0, 1)
+    with pytest.raises(nl.NLSE2SHOCError):
+        S.rk4(psi, float("nan"), 1)
+    with pytest.raises(nl.NLSE2SHOCError):
+        S.laplacian(psi, out=psi)
+    flat = torch.zeros(psi.numel() + 1, dtype=psi.dtype, device="cuda")
+    with pytest.raises(nl.NLSE2SHOCError):  # 8-byte aligned only
+        S.rk4(flat[1:].view(psi.shape), 1e-3, 1)
+    bad = psi.clone()
+    bad.view(-1)[17] = complex(float("nan"), 0.0)
+    with pytest.raises(nl.NLSE2SHOCError):
+        S.check_finite(bad)
+    S.check_finite(psi)
+
+
+def test_dirichlet_boundary_values_are_bit_exact():
+    """`dbc_ut`: Psi_t,b = 0, so boundary values never change, to the bit."""
+    w = _small(3, (37, 19, 9), "dirichlet", "c128", "harmonic")
+    S = H.gpu_solver(w, "c128")
+    psi = H.psi0_host(w, "c128")
+    g = _dev(psi)
+    S.rk4(g, 1e-4, 7)
+    out = g.cpu().numpy()
+    m = np.ones(psi.shape, bool)
+    m[1:-1, 1:-1, 1:-1] = False
+    assert np.array_equal(out[m], psi[m])
+
+
+# --------------------------------------------------------------------------- configs
+def test_C1_full_2000_steps_and_exact_soliton():
+    w = configs.C1()
+    S = H.gpu_solver(w, "c128")
+    psi = H.psi0_host(w, "c128")
+    P = H.oracle_problem(w)
+    kmax = oracle.kmax(P, psi)
+    assert abs(S.stability_bound(_dev(psi)) - kmax) <= 1e-13 * kmax
+    dt = 0.4 * kmax
+    g = _dev(psi)
+    S.rk4(g, dt, w["steps"])
+    ref = oracle.rk4(P, psi, dt, w["steps"])
+    out = g.cpu().numpy()
+    assert H.rel_l2(out, ref) <= 1e-12
+    # exact bright soliton sqrt2 sech(x) e^{it} (north star); magnitude of the 4th-order error
+    ic = dict(w["ic"])
+    ic["p"] = [math.sqrt(2.0), 1.0, dt * w["steps"]]
+    import icgen
+
+    ex = icgen.fill(ic, w["grid"])
+    assert H.rel_l2(out, ex) < 3e-7
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_C2_full_size_20_steps(dtype):
+    w = configs.C2()
+    psi = H.psi0_host(w, dtype)
+    P = H.oracle_problem(w)
+    dt = 0.8 * oracle.kmax(P, psi.astype(np.complex128))
+    S = H.gpu_solver(w, dtype)
+    g = _dev(psi)
+    S.rk4(g, dt, 20)
+    ref = oracle.rk4(P, psi.astype(np.complex128), dt, 20)
+    assert H.rel_l2(g.cpu().numpy(), ref) <= H.TOL[dtype]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_C2_full_500_steps(dtype):
+    w = configs.C2()
+    psi = H.psi0_host(w, dtype)
+    P = H.oracle_problem(w)
+    dt = 0.8 * oracle.kmax(P, psi.astype(np.complex128))
+    S = H.gpu_solver(w, dtype)
+    g = _dev(psi)
+    S.rk4(g, dt, w["steps"])
+    ref = oracle.rk4(P, psi.astype(np.complex128), dt, w["steps"])
+    assert H.rel_l2(g.cpu().numpy(), ref) <= H.TOL[dtype]
+
+
+def _crop_parity(w, dtype, nsteps, targets, tol):
+    """Full-size GPU run in the bench launch configuration; sampled target boxes checked
+    against oracle runs on their dependency-cone crops (bitwise equal to the full oracle
+    inside the target), with the full-domain dt."""
+    dims = w["grid"]["dims"]
+    kmax = H.oracle_kmax_full(w, dtype)
+    dt = 0.8 * kmax
+    S = H.gpu_solver(w, dtype)
+    g = torch.empty(tuple(reversed(w["grid"]["n"][:dims])), dtype=H.torch_dtype(dtype))
+    import icgen
+
+    icgen.fill(w["ic"], w["grid"], dtype=H.NP[dtype], out=g.numpy())
+    g = g.cuda()
+    kg = S.stability_bound(g)
+    assert abs(kg - kmax) <= (1e-6 if dtype == "c64" else 1e-13) * kmax
+    S.rk4(g, dt, nsteps)
+    torch.cuda.synchronize()
+    for tlo, tcnt in targets:
+        lo, cnt = H.crop_box(w, tlo, tcnt, nsteps)
+        psi = H.psi0_host(w, dtype, lo, cnt).astype(np.complex128)
+        ref = oracle.rk4(H.oracle_problem(w, lo, cnt), psi, dt, nsteps)
+        rel_lo = [tlo[d] - lo[d] for d in range(3)]
+        want = ref[H.sl(dims, rel_lo, tcnt)]
+        got = g[H.sl(dims, tlo, tcnt)].cpu().numpy()
+        assert H.rel_l2(got, want) <= tol, (tlo, tcnt)
+    del g
+    S.close()
+    torch.cuda.empty_cache()
+
+
+def test_C3_full_size_crops():
+    w = configs.C3()
+    n = 8192
+    T = [([0, 0, 0], [48, 48, 1]), ([4000, 4100, 0], [64, 40, 1]), ([n - 40, n - 33, 0], [40, 33, 1]),
+         ([0, 2000, 0], [20, 64, 1])]
+    _crop_parity(w, "c128", 4, T, 1e-12)
+
+
+def test_C4_full_size_crops():
+    w = configs.C4()
+    n = 768
+    T = [([0, 0, 0], [24, 20, 18]), ([370, 380, 384], [40, 24, 16]), ([n - 20, n - 17, n - 22], [20, 17, 22]),
+         ([100, 0, 700], [70, 16, 9]), ([0, 400, 0], [9, 33, 20])]
+    _crop_parity(w, "c64", 2, T, 1e-5)
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_C5W_full_size_crops(dtype):
+    w = configs.C5W(1)
+    T = [([0, 0, 0], [20, 20, 20]), ([380, 370, 90], [30, 30, 12]), ([748, 750, 176], [20, 18, 16])]
+    _crop_parity(w, dtype, 2, T, H.TOL[dtype])
