@@ -36,8 +36,10 @@ def needs_build():
     return any(os.path.getmtime(s) > t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Compile libnlse2shoc.so (or `out`, with extra -D `defines`, for experiments)."""
+    target = out or SO
+    if not force and out is None and not needs_build():
         return SO
     nvcc = os.environ.get("NVCC", "nvcc")
     cmd = [nvcc, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
@@ -47,16 +49,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd += ["-I", os.path.join(nd, "include"), "-DNLSE_WITH_NCCL"]
     if verbose:
         cmd += ["-Xptxas", "-v"]
-    cmd += ["-o", SO + ".tmp", SRC]
+    cmd += [f"-D{d}" for d in defines]
+    cmd += ["-o", target + ".tmp", SRC]
     if nd:
         cmd += ["-L", os.path.join(nd, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath," + os.path.join(nd, "lib")]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
-    os.replace(SO + ".tmp", SO)
+    os.replace(target + ".tmp", target)
     if verbose:
         sys.stdout.write(r.stdout + r.stderr)
-    return SO
+    return target
 
 
 if __name__ == "__main__":

@@ -9,7 +9,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "libnlse2shoc.so")
+SO_PATH = os.environ.get("NLSE_LIB") or os.path.join(_HERE, "libnlse2shoc.so")
 
 OK, EINVAL, ENOMEM, ECUDA, ENCCL, ENONFINITE, EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
 BC = {"dirichlet": 0, "lapzero": 1}

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -107,7 +108,8 @@ static bool finite_pos(double v) { return std::isfinite(v) && v > 0.0; }
 
 static nlse2shoc_status encode_map(CUtensorMap *tm, void *base, int dims_tensor, uint64_t inner_elems8,
                                    uint64_t rows, uint64_t planes, uint64_t pitch_bytes, uint64_t plane_bytes,
-                                   uint32_t box0, uint32_t box1) {
+                                   uint32_t box0, uint32_t box1,
+                                   CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
   auto enc = get_encode();
   if (!enc) return fail(NLSE2SHOC_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t gdim[3] = {inner_elems8, rows, planes};
@@ -115,10 +117,20 @@ static nlse2shoc_status encode_map(CUtensorMap *tm, void *base, int dims_tensor,
   cuuint32_t box[3] = {box0, box1, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, dims_tensor, base, gdim, gstr, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(NLSE2SHOC_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
   return NLSE2SHOC_OK;
+}
+
+// L2 promotion of the stencil-input (halo) boxes; NLSE_TMA_PROMO=0/64/128/256 overrides
+// (default none: a halo sector miss then fetches 32 B instead of a 256 B granule).
+static CUtensorMapL2promotion tma_promo() {
+  const char *e = getenv("NLSE_TMA_PROMO");
+  int v = e ? atoi(e) : 0;
+  return v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                 : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                            : v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_NONE;
 }
 
 template <int DIMS, typename R> struct Maps {
@@ -129,9 +141,9 @@ template <int DIMS, typename R> struct Maps {
     const uint64_t S = sizeof(cplx<R>);
     if (DIMS == 3)
       return encode_map(tm, base, 3, uint64_t(H->nx) * LY::EPC, uint64_t(H->ny), uint64_t(planes), H->pitch * S,
-                        H->plane * S, LY::BW, LY::SROWS);
+                        H->plane * S, LY::BW, LY::SROWS, tma_promo());
     return encode_map(tm, base, 2, uint64_t(H->nx) * LY::EPC, uint64_t(planes), 1, H->pitch * S, H->pitch * S * planes,
-                      LY::BW, 1);
+                      LY::BW, 1, tma_promo());
   }
   // pointwise (Psi^n / acc) map: tile box without halo
   static nlse2shoc_status point(nlse2shoc_t H, CUtensorMap *tm, void *base) {
@@ -162,6 +174,8 @@ template <typename R> static void fill_params(nlse2shoc_t H, StageParams<R> &P) 
   P.cx = R(1.0 / (12.0 * hx * hx));
   P.cy = R(1.0 / (12.0 * hy * hy));
   P.cz = R(1.0 / (12.0 * hz * hz));
+  P.c30 = R(30.0 * (1.0 / (12.0 * hx * hx) + (H->dims == 3 ? 1.0 / (12.0 * hy * hy) : 0.0) +
+                    (H->dims >= 2 ? 1.0 / (12.0 * hz * hz) : 0.0)));
   P.ihx2 = R(1.0 / (hx * hx));
   P.ihy2 = R(1.0 / (hy * hy));
   P.ihz2 = R(1.0 / (hz * hz));

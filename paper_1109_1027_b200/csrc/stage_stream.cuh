@@ -20,6 +20,8 @@
 // L2).  Shard seams (multi-GPU z-slabs) read their two halo planes through extra tensor
 // maps pointing at the halo buffers the NCCL exchange filled.
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace nlse {
@@ -30,18 +32,41 @@ enum Mode { M_S1 = 1, M_S2 = 2, M_S3 = 3, M_S4 = 4, M_LAP = 5 };
 // (tile + 2+2 halo, rounded so that it splits into NBOX equal TMA boxes); every TMA
 // destination must be 128-byte aligned, so box and slot byte sizes are multiples of 128,
 // and a box's inner extent must stay <= 256 eight-byte elements.
+// Ring depths per stage kind: RTn = stencil-input slots and RPn = Psi^n/acc slots when the
+// stage streams n pointwise tiles (n = 0: stage 1 and the Laplacian; 1: stage 4; 2: stages
+// 2-3).  The pinned window of the T ring is planes k-2..k+2; the rest is prefetch, sized so
+// that each SM keeps ~100-200 KB of TMA loads in flight.
 template <int DIMS, typename R> struct Cfg;
+#ifndef NLSE_CFG3F
+#define NLSE_CFG3F 0
+#endif
+#if NLSE_CFG3F == 3
 template <> struct Cfg<3, float> {
-  static constexpr int TX = 64, TY = 16, PPX = 2, RPW = 2, NCW = 8, RT = 8, RP = 4, NBOX = 1, NBOXP = 1, W = 68;
+  static constexpr int TX = 64, TY = 24, PPX = 2, RPW = 1, NCW = 24, NBOX = 1, NBOXP = 1, W = 68;
+  static constexpr int RT0 = 13, RT1 = 8, RP1 = 6, RT2 = 7, RP2 = 3;
 };
+#elif NLSE_CFG3F == 2
+template <> struct Cfg<3, float> {
+  static constexpr int TX = 64, TY = 16, PPX = 2, RPW = 2, NCW = 8, NBOX = 1, NBOXP = 1, W = 68;
+  static constexpr int RT0 = 18, RT1 = 10, RP1 = 10, RT2 = 9, RP2 = 5;
+};
+#else
+template <> struct Cfg<3, float> {
+  static constexpr int TX = 64, TY = 16, PPX = 2, RPW = 1, NCW = 16, NBOX = 1, NBOXP = 1, W = 68;
+  static constexpr int RT0 = 18, RT1 = 10, RP1 = 10, RT2 = 9, RP2 = 5;
+};
+#endif
 template <> struct Cfg<3, double> {
-  static constexpr int TX = 32, TY = 16, PPX = 1, RPW = 2, NCW = 8, RT = 8, RP = 4, NBOX = 1, NBOXP = 1, W = 36;
+  static constexpr int TX = 32, TY = 16, PPX = 1, RPW = 1, NCW = 16, NBOX = 1, NBOXP = 1, W = 36;
+  static constexpr int RT0 = 18, RT1 = 10, RP1 = 10, RT2 = 9, RP2 = 5;
 };
 template <> struct Cfg<2, float> {
-  static constexpr int TX = 512, TY = 1, PPX = 2, RPW = 1, NCW = 8, RT = 12, RP = 6, NBOX = 3, NBOXP = 2, W = 528;
+  static constexpr int TX = 512, TY = 1, PPX = 2, RPW = 1, NCW = 8, NBOX = 3, NBOXP = 2, W = 528;
+  static constexpr int RT0 = 40, RT1 = 24, RP1 = 20, RT2 = 20, RP2 = 12;
 };
 template <> struct Cfg<2, double> {
-  static constexpr int TX = 256, TY = 1, PPX = 1, RPW = 1, NCW = 8, RT = 12, RP = 6, NBOX = 3, NBOXP = 2, W = 264;
+  static constexpr int TX = 256, TY = 1, PPX = 1, RPW = 1, NCW = 8, NBOX = 3, NBOXP = 2, W = 264;
+  static constexpr int RT0 = 40, RT1 = 24, RP1 = 20, RT2 = 20, RP2 = 12;
 };
 
 template <typename R> struct StageParams {
@@ -54,6 +79,7 @@ template <typename R> struct StageParams {
   int64_t pitch;         // elements per x-row (all buffers)
   int64_t plane;         // elements per plane = pitch * ny
   R cx, cy, cz;          // 1/(12 h^2) per axis (wide-stencil scale)
+  R c30;                 // 30 (cx + cy + cz): centre weight of the summed wide stencil
   R ihx2, ihy2, ihz2;    // 1/h^2 per axis (delta^2 in the face rule)
   R hx2, hy2, hz2;       // h^2 per axis (ghost formula)
   R a, s, inv_a;
@@ -90,9 +116,15 @@ template <int DIMS, typename R> struct Layout {
   template <int MODE> __host__ __device__ static constexpr bool needs_psi() { return MODE == M_S2 || MODE == M_S3; }
   template <int MODE> __host__ __device__ static constexpr bool needs_acc() { return MODE == M_S2 || MODE == M_S3 || MODE == M_S4; }
   template <int MODE> __host__ __device__ static constexpr int pa_tiles() { return (needs_psi<MODE>() ? 1 : 0) + (needs_acc<MODE>() ? 1 : 0); }
+  template <int MODE> __host__ __device__ static constexpr int rt() {
+    return pa_tiles<MODE>() == 0 ? C::RT0 : (pa_tiles<MODE>() == 1 ? C::RT1 : C::RT2);
+  }
+  template <int MODE> __host__ __device__ static constexpr int rp() {
+    return pa_tiles<MODE>() == 0 ? 0 : (pa_tiles<MODE>() == 1 ? C::RP1 : C::RP2);
+  }
   template <int MODE> __host__ __device__ static constexpr size_t smem_bytes() {
-    return 128 + size_t(C::RT) * SLOT_BYTES + size_t(pa_tiles<MODE>() ? C::RP : 0) * 2 * PTILE_BYTES +
-           size_t(2 * C::RT + 2 * C::RP) * 8;
+    return size_t(rt<MODE>()) * SLOT_BYTES + size_t(rp<MODE>()) * pa_tiles<MODE>() * PTILE_BYTES +
+           size_t(2 * rt<MODE>() + 2 * rp<MODE>()) * 8;
   }
 };
 
@@ -154,18 +186,22 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
   using CT = cplx<R>;
   constexpr int HY = LY::HY, W = C::W, TX = C::TX, TY = C::TY;
   constexpr int NPA = LY::template pa_tiles<MODE>();
-  constexpr int RP = NPA ? C::RP : 0;
+  constexpr int RT = LY::template rt<MODE>(), RP = LY::template rp<MODE>();
+  constexpr int RPM = RP > 0 ? RP : 1;  // modulus for the (unused when RP = 0) P-ring counters
+  constexpr int ACC_OFF = LY::template needs_psi<MODE>() ? LY::PTILE : 0;  // acc tile offset in a P slot
 
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  // Dynamic shared memory starts 1 KB-aligned; deriving every pointer from smem_raw by
+  // plain offsets keeps them in the shared state space (LDS, 32-bit addressing).
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char *base = smem_raw;
   CT *ring = reinterpret_cast<CT *>(base);
-  CT *pring = reinterpret_cast<CT *>(base + size_t(C::RT) * LY::SLOT_BYTES);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(base + size_t(C::RT) * LY::SLOT_BYTES + size_t(RP) * 2 * LY::PTILE_BYTES);
-  uint64_t *fullT = bars, *emptyT = bars + C::RT, *fullP = bars + 2 * C::RT, *emptyP = bars + 2 * C::RT + C::RP;
+  CT *pring = reinterpret_cast<CT *>(base + size_t(RT) * LY::SLOT_BYTES);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(base + size_t(RT) * LY::SLOT_BYTES + size_t(RP) * NPA * LY::PTILE_BYTES);
+  uint64_t *fullT = bars, *emptyT = bars + RT, *fullP = bars + 2 * RT, *emptyP = bars + 2 * RT + RP;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < C::RT; ++i) {
+    for (int i = 0; i < RT; ++i) {
       mbar_init(&fullT[i], 1);
       mbar_init(&emptyT[i], C::NCW);
     }
@@ -191,14 +227,17 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
         if (LY::template needs_psi<MODE>()) prefetch_tmap(&tm_psi);
         if (LY::template needs_acc<MODE>()) prefetch_tmap(&tm_acc);
       }
+      // stencil-input planes are re-read (halos) by neighbouring tiles: keep them in L2;
+      // Psi^n / acc tiles are read exactly once: evict first.
+      const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
       uint32_t tcnt = 0, pcnt = 0;
       for (int t = blockIdx.x; t < P.ntiles; t += G) {
         const int chunk = t / ncol, col = t % ncol;
         const int x0 = (col % P.ncx) * TX, y0 = (col / P.ncx) * TY;
         const int kb = chunk * chunk_len, ke = min(P.nz, kb + chunk_len);
         auto produceT = [&](int p) {
-          const uint32_t slot = tcnt % C::RT, par = (tcnt / C::RT) & 1;
-          mbar_wait(&emptyT[slot], par ^ 1);
+          const uint32_t slot = tcnt % RT, par = (tcnt / RT) & 1;
+          mbar_wait_backoff(&emptyT[slot], par ^ 1);
           const CUtensorMap *m = nullptr;
           int pz = p;
           if (p >= 0 && p < P.nz) m = &tm_T;
@@ -210,8 +249,9 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
 #pragma unroll
             for (int b = 0; b < C::NBOX; ++b) {
               const int c0 = (x0 - 2) * LY::EPC + b * LY::BW;
-              if (DIMS == 3) tma_load_3d(reinterpret_cast<char *>(dst) + b * LY::BW * 8, m, &fullT[slot], c0, y0 - 2, pz);
-              else tma_load_2d(reinterpret_cast<char *>(dst) + b * LY::BW * 8, m, &fullT[slot], c0, pz);
+              if (DIMS == 3)
+                tma_load_3d_hint(reinterpret_cast<char *>(dst) + b * LY::BW * 8, m, &fullT[slot], c0, y0 - 2, pz, pol_keep);
+              else tma_load_2d_hint(reinterpret_cast<char *>(dst) + b * LY::BW * 8, m, &fullT[slot], c0, pz, pol_keep);
             }
           } else {
             mbar_arrive(&fullT[slot]);
@@ -219,10 +259,10 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
           ++tcnt;
         };
         auto produceP = [&](int k) {
-          const uint32_t slot = pcnt % C::RP, par = (pcnt / C::RP) & 1;
-          mbar_wait(&emptyP[slot], par ^ 1);
+          const uint32_t slot = pcnt % RPM, par = (pcnt / RPM) & 1;
+          mbar_wait_backoff(&emptyP[slot], par ^ 1);
           mbar_arrive_expect_tx(&fullP[slot], NPA * LY::PTILE_BYTES);
-          CT *dst = pring + size_t(slot) * 2 * LY::PTILE;
+          CT *dst = pring + size_t(slot) * NPA * LY::PTILE;
 #pragma unroll
           for (int q = 0; q < 2; ++q) {
             const bool want = q == 0 ? LY::template needs_psi<MODE>() : LY::template needs_acc<MODE>();
@@ -231,9 +271,9 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
 #pragma unroll
             for (int b = 0; b < C::NBOXP; ++b) {
               const int c0 = x0 * LY::EPC + b * LY::BWP;
-              char *d = reinterpret_cast<char *>(dst + q * LY::PTILE) + b * LY::BWP * 8;
-              if (DIMS == 3) tma_load_3d(d, m, &fullP[slot], c0, y0, k);
-              else tma_load_2d(d, m, &fullP[slot], c0, k);
+              char *d = reinterpret_cast<char *>(dst + (q == 0 ? 0 : ACC_OFF)) + b * LY::BWP * 8;
+              if (DIMS == 3) tma_load_3d_hint(d, m, &fullP[slot], c0, y0, k, pol_stream);
+              else tma_load_2d_hint(d, m, &fullP[slot], c0, k, pol_stream);
             }
           }
           ++pcnt;
@@ -249,190 +289,252 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
   }
 
   // -------------------------------------------------------------------- consumer warps
+  // Each consumer thread owns PPX consecutive x-points in RPW rows of the tile.  Values of
+  // its own column at planes k-2, k-1, k+1 live in a register queue (qm2, qm1, qp1); plane
+  // k+2 is read once from its slot; x / y neighbours come from slot k.  Ring slots and
+  // barrier parities advance with running counters (no per-plane division).
   const int ct = threadIdx.x;                      // 0 .. NCW*32-1
-  constexpr int CPT = TX / C::PPX;                 // column groups per row
+  constexpr int PPX = C::PPX, RPW = C::RPW;
+  constexpr int CPT = TX / PPX;                    // column groups per row
   const int cg = ct % CPT, rg = ct / CPT;
-  const int lx0 = cg * C::PPX;                     // first local x of this thread
-  const int ly0 = rg * C::RPW;                     // first local row of this thread
+  const int lx0 = cg * PPX;                        // first local x of this thread
+  const int ly0 = rg * RPW;                        // first local row of this thread
+  const CT zero = mk<R>(R(0), R(0));
+  const R cx = P.cx, cy = P.cy, cz = P.cz, c30 = P.c30, pa_ = P.a, ps_ = P.s, ca = P.ca, cb = P.cb;
+  const int nx = P.nx, ny = P.ny, nz = P.nz, NZ = P.NZ, z0 = P.z0;
   uint32_t tcnt = 0, pcnt = 0;
+  auto inc = [](int v, int m) { return v + 1 == m ? 0 : v + 1; };
 
   for (int t = blockIdx.x; t < P.ntiles; t += G) {
     const int chunk = t / ncol, col = t % ncol;
     const int x0 = (col % P.ncx) * TX, y0 = (col / P.ncx) * TY;
-    const int kb = chunk * chunk_len, ke = min(P.nz, kb + chunk_len);
+    const int kb = chunk * chunk_len, ke = min(nz, kb + chunk_len);
     const uint32_t tbase = tcnt;  // ring counter of plane kb-2
-    auto tslot = [&](int p) -> CT * { return ring + size_t((tbase + uint32_t(p - kb + 2)) % C::RT) * LY::SLOT; };
+    auto tslot = [&](int p) -> CT * { return ring + size_t((tbase + uint32_t(p - kb + 2)) % RT) * LY::SLOT; };
     auto twait = [&](int p) {
       const uint32_t c = tbase + uint32_t(p - kb + 2);
-      mbar_wait(&fullT[c % C::RT], (c / C::RT) & 1);
+      mbar_wait(&fullT[c % RT], (c / RT) & 1);
     };
-    auto trelease = [&](int p) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&emptyT[(tbase + uint32_t(p - kb + 2)) % C::RT]);
-    };
-    for (int p = kb - 2; p < kb + 2; ++p) twait(p);
 
     // tile facts (CTA-uniform)
-    const bool xlo = x0 == 0, xhi = (x0 <= P.nx - 2) && (P.nx - 2 < x0 + TX);
-    const bool ylo = DIMS == 3 && y0 == 0, yhi = DIMS == 3 && (y0 <= P.ny - 2) && (P.ny - 2 < y0 + TY);
+    const bool xlo = x0 == 0, xhi = (x0 <= nx - 2) && (nx - 2 < x0 + TX);
+    const bool ylo = DIMS == 3 && y0 == 0, yhi = DIMS == 3 && (y0 <= ny - 2) && (ny - 2 < y0 + TY);
+    const bool inner_xy = x0 >= 1 && x0 + TX <= nx - 1 && (DIMS == 2 || (y0 >= 1 && y0 + TY <= ny - 1));
+
+    // per-thread potential tables of this tile (harmonic V is separable)
+    R vxr[PPX], vyr[RPW];
+#pragma unroll
+    for (int q = 0; q < PPX; ++q) vxr[q] = (P.vkind == 1 && x0 + lx0 + q < nx) ? P.vx[x0 + lx0 + q] : R(0);
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) vyr[r] = (P.vkind == 1 && P.vy && y0 + ly0 + r < ny) ? P.vy[y0 + ly0 + r] : R(0);
+
+    const int toff = (ly0 + HY) * W + lx0;  // this thread's first row/col in a T slot
+    auto centre = [&](const CT *slot, int r, CT *out) { lds_run<R, PPX>(slot + toff + r * W + 2, out); };
+    CT qm2[RPW][PPX], qm1[RPW][PPX], qp1[RPW][PPX];
+    for (int p = kb - 2; p < kb + 2; ++p) twait(p);
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+      centre(tslot(kb - 2), r, qm2[r]);
+      centre(tslot(kb - 1), r, qm1[r]);
+      centre(tslot(kb + 1), r, qp1[r]);
+    }
+    // running ring state: slots of planes k, k+2, k-2; parity of plane k+2; P ring
+    int sk = int((tbase + 2) % RT), sk2 = int((tbase + 4) % RT), skm2 = int(tbase % RT);
+    uint32_t ph2 = ((tbase + 4) / RT) & 1;
+    int sp = int(pcnt % RPM);
+    uint32_t php = (pcnt / RPM) & 1;
+    cplx<R> *outT = P.out_T + int64_t(kb) * P.plane + int64_t(y0 + ly0) * P.pitch + (x0 + lx0);
+    cplx<R> *outA = (MODE != M_LAP && MODE != M_S4) ? P.out_acc + (outT - P.out_T) : nullptr;
 
     for (int k = kb; k < ke; ++k) {
-      twait(k + 2);
-      CT *pa = nullptr;
+      const int gz = z0 + k;  // global streamed index
+      const R vzk = (P.vkind == 1 && P.vz) ? P.vz[gz] : R(0);
+      mbar_wait(&fullT[sk2], ph2);
+      const CT *pa = nullptr;
       if (NPA) {
-        const uint32_t slot = pcnt % C::RP;
-        mbar_wait(&fullP[slot], (pcnt / C::RP) & 1);
-        pa = pring + size_t(slot) * 2 * LY::PTILE;
+        mbar_wait(&fullP[sp], php);
+        pa = pring + size_t(sp) * NPA * LY::PTILE;
       }
-      const int gz = P.z0 + k;  // global streamed index
-      const bool zint = gz >= 1 && gz <= P.NZ - 2;
-      const bool zg_lo = P.lo_face && k == 1;
-      const bool zg_hi = P.hi_face && k == P.nz - 2;
-      const bool do_ghost = (zint && (xlo || xhi || ylo || yhi)) || zg_lo || zg_hi;
+      const bool zint = gz >= 1 && gz <= NZ - 2;
+      const bool fast = inner_xy && zint && gz >= 2 && gz <= NZ - 3;  // no boundary point, no ghost
 
-      if (do_ghost) {
-        // ---- ghost values (reading R8/R9, ghost form): one per face point that a depth-1
-        // interior point of this tile/plane reads.
-        CT *s0 = tslot(k), *sm = tslot(k - 1), *sp = tslot(k + 1);
-        auto at = [&](CT *s, int lx, int ly) -> CT & { return s[(ly + HY) * W + lx + 2]; };
-        if (zint) {
-          // x faces: rows of the tile (3D: interior rows only)
-          for (int task = ct; task < 2 * TY; task += C::NCW * 32) {
-            const bool hi = task >= TY;
-            if (hi ? !xhi : !xlo) continue;
-            const int ly = task % TY, gy = y0 + ly;
-            if (DIMS == 3 && (gy < 1 || gy > P.ny - 2)) continue;
-            if (gy >= P.ny) continue;
-            const int bx = hi ? P.nx - 1 : 0, lb = bx - x0, n = hi ? -1 : 1;
-            CT cb = at(s0, lb, ly), cin = at(s0, lb + n, ly);
-            CT D = lambda_b(P, cb, potential(P, bx, gy, k));
-            D = D - d2(at(sm, lb, ly), cb, at(sp, lb, ly), P.ihz2);
-            if (DIMS == 3) D = D - d2(at(s0, lb, ly - 1), cb, at(s0, lb, ly + 1), P.ihy2);
-            at(s0, lb - n, ly) = axpy(R(2) * cb - cin, P.hx2, D);
-          }
-          if (DIMS == 3) {
-            for (int task = ct; task < 2 * TX; task += C::NCW * 32) {
-              const bool hi = task >= TX;
-              if (hi ? !yhi : !ylo) continue;
-              const int lx = task % TX, gx = x0 + lx;
-              if (gx < 1 || gx > P.nx - 2) continue;
-              const int by = hi ? P.ny - 1 : 0, lb = by - y0, n = hi ? -1 : 1;
-              CT cb = at(s0, lx, lb), cin = at(s0, lx, lb + n);
-              CT D = lambda_b(P, cb, potential(P, gx, by, k));
-              D = D - d2(at(sm, lx, lb), cb, at(sp, lx, lb), P.ihz2);
-              D = D - d2(at(s0, lx - 1, lb), cb, at(s0, lx + 1, lb), P.ihx2);
-              at(s0, lx, lb - n) = axpy(R(2) * cb - cin, P.hy2, D);
+      if (!fast) {
+        const bool zg_lo = P.lo_face && k == 1;
+        const bool zg_hi = P.hi_face && k == nz - 2;
+        const bool do_ghost = (zint && (xlo || xhi || ylo || yhi)) || zg_lo || zg_hi;
+        if (do_ghost) {
+          // ---- ghost values (reading R8/R9, ghost form): one per face point that a depth-1
+          // interior point of this tile/plane reads.
+          CT *s0 = tslot(k), *sm = tslot(k - 1), *spp = tslot(k + 1);
+          auto at = [&](CT *s_, int lx, int ly) -> CT & { return s_[(ly + HY) * W + lx + 2]; };
+          if (zint) {
+            // x faces: rows of the tile (3D: interior rows only)
+            for (int task = ct; task < 2 * TY; task += C::NCW * 32) {
+              const bool hi = task >= TY;
+              if (hi ? !xhi : !xlo) continue;
+              const int ly = task % TY, gy = y0 + ly;
+              if (DIMS == 3 && (gy < 1 || gy > ny - 2)) continue;
+              if (gy >= ny) continue;
+              const int bx = hi ? nx - 1 : 0, lb = bx - x0, n = hi ? -1 : 1;
+              CT cbv = at(s0, lb, ly), cin = at(s0, lb + n, ly);
+              CT D = lambda_b(P, cbv, potential(P, bx, gy, k));
+              D = D - d2(at(sm, lb, ly), cbv, at(spp, lb, ly), P.ihz2);
+              if (DIMS == 3) D = D - d2(at(s0, lb, ly - 1), cbv, at(s0, lb, ly + 1), P.ihy2);
+              at(s0, lb - n, ly) = axpy(R(2) * cbv - cin, P.hx2, D);
+            }
+            if (DIMS == 3) {
+              for (int task = ct; task < 2 * TX; task += C::NCW * 32) {
+                const bool hi = task >= TX;
+                if (hi ? !yhi : !ylo) continue;
+                const int lx = task % TX, gx = x0 + lx;
+                if (gx < 1 || gx > nx - 2) continue;
+                const int by = hi ? ny - 1 : 0, lb = by - y0, n = hi ? -1 : 1;
+                CT cbv = at(s0, lx, lb), cin = at(s0, lx, lb + n);
+                CT D = lambda_b(P, cbv, potential(P, gx, by, k));
+                D = D - d2(at(sm, lx, lb), cbv, at(spp, lx, lb), P.ihz2);
+                D = D - d2(at(s0, lx - 1, lb), cbv, at(s0, lx + 1, lb), P.ihx2);
+                at(s0, lx, lb - n) = axpy(R(2) * cbv - cin, P.hy2, D);
+              }
             }
           }
-        }
-        if (zg_lo || zg_hi) {
-          // streamed-axis face: ghost plane -1 (before output plane 1) or nz (before nz-2)
-          const int bz = zg_lo ? 0 : P.nz - 1, n = zg_lo ? 1 : -1;
-          CT *sb = tslot(bz), *si = tslot(bz + n), *sg = tslot(bz - n);
-          for (int task = ct; task < TX * TY; task += C::NCW * 32) {
-            const int lx = task % TX, ly = task / TX, gx = x0 + lx, gy = y0 + ly;
-            if (gx < 1 || gx > P.nx - 2) continue;
-            if (DIMS == 3 && (gy < 1 || gy > P.ny - 2)) continue;
-            CT cb = at(sb, lx, ly), cin = at(si, lx, ly);
-            CT D = lambda_b(P, cb, potential(P, gx, gy, bz));
-            D = D - d2(at(sb, lx - 1, ly), cb, at(sb, lx + 1, ly), P.ihx2);
-            if (DIMS == 3) D = D - d2(at(sb, lx, ly - 1), cb, at(sb, lx, ly + 1), P.ihy2);
-            at(sg, lx, ly) = axpy(R(2) * cb - cin, P.hz2, D);
+          if (zg_lo || zg_hi) {
+            // streamed-axis face: ghost plane -1 (before output plane 1) or nz (before nz-2)
+            const int bz = zg_lo ? 0 : nz - 1, n = zg_lo ? 1 : -1;
+            CT *sb = tslot(bz), *si = tslot(bz + n), *sg = tslot(bz - n);
+            for (int task = ct; task < TX * TY; task += C::NCW * 32) {
+              const int lx = task % TX, ly = task / TX, gx = x0 + lx, gy = y0 + ly;
+              if (gx < 1 || gx > nx - 2) continue;
+              if (DIMS == 3 && (gy < 1 || gy > ny - 2)) continue;
+              CT cbv = at(sb, lx, ly), cin = at(si, lx, ly);
+              CT D = lambda_b(P, cbv, potential(P, gx, gy, bz));
+              D = D - d2(at(sb, lx - 1, ly), cbv, at(sb, lx + 1, ly), P.ihx2);
+              if (DIMS == 3) D = D - d2(at(sb, lx, ly - 1), cbv, at(sb, lx, ly + 1), P.ihy2);
+              at(sg, lx, ly) = axpy(R(2) * cbv - cin, P.hz2, D);
+            }
+          }
+          fence_proxy_async_smem();  // generic writes to slots precede later TMA refills
+          named_bar_sync(1, C::NCW * 32);
+          if (zg_lo) {
+#pragma unroll
+            for (int r = 0; r < RPW; ++r) centre(tslot(-1), r, qm2[r]);
           }
         }
-        fence_proxy_async_smem();  // generic writes to slots precede later TMA refills
-        named_bar_sync(1, C::NCW * 32);
       }
 
       // ---- stencil + RHS + stage combine for this thread's points of plane k
-      const CT *s0 = tslot(k), *sm1 = tslot(k - 1), *sp1 = tslot(k + 1), *sm2 = tslot(k - 2), *sp2 = tslot(k + 2);
+      const CT *s0 = ring + size_t(sk) * LY::SLOT + toff, *sp2 = ring + size_t(sk2) * LY::SLOT + toff;
 #pragma unroll
-      for (int r = 0; r < C::RPW; ++r) {
-        const int ly = ly0 + r, gy = y0 + ly;
-        const int srow = (ly + HY) * W;
-        CT run[C::PPX + 4];
-        lds_run<R, C::PPX + 4>(s0 + srow + lx0, run);
-        CT zm2[C::PPX], zm1[C::PPX], zp1[C::PPX], zp2[C::PPX];
-        lds_run<R, C::PPX>(sm2 + srow + lx0 + 2, zm2);
-        lds_run<R, C::PPX>(sm1 + srow + lx0 + 2, zm1);
-        lds_run<R, C::PPX>(sp1 + srow + lx0 + 2, zp1);
-        lds_run<R, C::PPX>(sp2 + srow + lx0 + 2, zp2);
-        CT ym2[C::PPX], ym1[C::PPX], yp1[C::PPX], yp2[C::PPX];
+      for (int r = 0; r < RPW; ++r) {
+        const int gy = y0 + ly0 + r;
+        CT run[PPX + 4];
+        lds_run<R, PPX + 4>(s0 + r * W, run);
+        CT zp2[PPX];
+        lds_run<R, PPX>(sp2 + r * W + 2, zp2);
+        CT ym2[PPX], ym1[PPX], yp1[PPX], yp2[PPX];
         if (DIMS == 3) {
-          lds_run<R, C::PPX>(s0 + srow - 2 * W + lx0 + 2, ym2);
-          lds_run<R, C::PPX>(s0 + srow - W + lx0 + 2, ym1);
-          lds_run<R, C::PPX>(s0 + srow + W + lx0 + 2, yp1);
-          lds_run<R, C::PPX>(s0 + srow + 2 * W + lx0 + 2, yp2);
+          lds_run<R, PPX>(s0 + (r - 2) * W + 2, ym2);
+          lds_run<R, PPX>(s0 + (r - 1) * W + 2, ym1);
+          lds_run<R, PPX>(s0 + (r + 1) * W + 2, yp1);
+          lds_run<R, PPX>(s0 + (r + 2) * W + 2, yp2);
         }
-        CT psv[C::PPX], acv[C::PPX];
-        if (LY::template needs_psi<MODE>()) lds_run<R, C::PPX>(pa + ly * TX + lx0, psv);
-        if (LY::template needs_acc<MODE>()) lds_run<R, C::PPX>(pa + LY::PTILE + ly * TX + lx0, acv);
+        CT psv[PPX], acv[PPX];
+        const int poff = (ly0 + r) * TX + lx0;
+        if (LY::template needs_psi<MODE>()) lds_run<R, PPX>(pa + poff, psv);
+        if (LY::template needs_acc<MODE>()) lds_run<R, PPX>(pa + ACC_OFF + poff, acv);
 
-        CT oT[C::PPX], oA[C::PPX];
-        bool valid[C::PPX];
+        CT oT[PPX], oA[PPX];
+        bool valid[PPX];
 #pragma unroll
-        for (int q = 0; q < C::PPX; ++q) {
+        for (int q = 0; q < PPX; ++q) {
           const int gx = x0 + lx0 + q;
-          valid[q] = gx < P.nx && gy < P.ny;
           const CT c = run[q + 2];
-          const bool bnd = gx == 0 || gx == P.nx - 1 || (DIMS == 3 && (gy == 0 || gy == P.ny - 1)) || gz == 0 ||
-                           gz == P.NZ - 1;
-          const R V = valid[q] ? potential(P, gx, gy, k) : R(0);
-          const R N = fma(P.s, norm2(c), -V);
-          CT F, L;
-          if (!bnd) {
-            // 5-point wide form per axis, (-g2 + 16 g1 - 30 g0 + 16 g-1 - g-2)/(12 h^2)
-            L = P.cx * (R(16) * (run[q + 1] + run[q + 3]) - (run[q] + run[q + 4]) - R(30) * c);
-            L = L + P.cz * (R(16) * (zm1[q] + zp1[q]) - (zm2[q] + zp2[q]) - R(30) * c);
-            if (DIMS == 3) L = L + P.cy * (R(16) * (ym1[q] + yp1[q]) - (ym2[q] + yp2[q]) - R(30) * c);
-            // F = i (a L + N c)
-            F = mk<R>(-fma(P.a, L.im, N * c.im), fma(P.a, L.re, N * c.re));
+          // 5-point wide form per axis, (16 (g-1 + g+1) - (g-2 + g+2) - 30 g0) / (12 h^2)
+          CT L = cx * (R(16) * (run[q + 1] + run[q + 3]) - (run[q] + run[q + 4]));
+          L = L + cz * (R(16) * (qm1[r][q] + qp1[r][q]) - (qm2[r][q] + zp2[q]));
+          if (DIMS == 3) L = L + cy * (R(16) * (ym1[q] + yp1[q]) - (ym2[q] + yp2[q]));
+          L = axpy(L, -c30, c);
+          R V;
+          if (P.vkind == 2) V = (gx < nx && gy < ny) ? potential(P, gx, gy, k) : R(0);
+          else V = (vxr[q] + vyr[r]) + vzk;
+          const R N = fma(ps_, norm2(c), -V);
+          CT F;
+          if (fast) {
+            valid[q] = true;
+            F = mk<R>(-fma(pa_, L.im, N * c.im), fma(pa_, L.re, N * c.re));  // i (a L + N c)
           } else {
-            L = lambda_b(P, c, V);
-            F = P.bc == 0 ? mk<R>(R(0), R(0)) : mk<R>(-(N * c.im), N * c.re);
+            valid[q] = gx < nx && gy < ny;
+            const bool bnd = gx == 0 || gx == nx - 1 || (DIMS == 3 && (gy == 0 || gy == ny - 1)) || !zint;
+            if (!bnd) {
+              F = mk<R>(-fma(pa_, L.im, N * c.im), fma(pa_, L.re, N * c.re));
+            } else {
+              L = lambda_b(P, c, V);
+              F = P.bc == 0 ? zero : mk<R>(-(N * c.im), N * c.re);
+            }
           }
           if (MODE == M_LAP) {
             oT[q] = L;
           } else if (MODE == M_S1) {
-            oA[q] = axpy(c, P.ca, F);
-            oT[q] = axpy(c, P.cb, F);
+            oA[q] = axpy(c, ca, F);
+            oT[q] = axpy(c, cb, F);
           } else if (MODE == M_S2 || MODE == M_S3) {
-            oA[q] = axpy(acv[q], P.ca, F);
-            oT[q] = axpy(psv[q], P.cb, F);
+            oA[q] = axpy(acv[q], ca, F);
+            oT[q] = axpy(psv[q], cb, F);
           } else {  // M_S4
-            oT[q] = axpy(acv[q], P.cb, F);
+            oT[q] = axpy(acv[q], cb, F);
           }
         }
         // ---- stores (128-bit when all PPX points are inside the grid)
-        const int64_t gidx = int64_t(k) * P.plane + int64_t(gy) * P.pitch + (x0 + lx0);
         using VV = V16<R>;
         bool all = true;
 #pragma unroll
-        for (int q = 0; q < C::PPX; ++q) all = all && valid[q];
+        for (int q = 0; q < PPX; ++q) all = all && valid[q];
+        cplx<R> *oTr = outT + int64_t(r) * P.pitch;
+        cplx<R> *oAr = (MODE != M_LAP && MODE != M_S4) ? outA + int64_t(r) * P.pitch : nullptr;
         if (all) {
 #pragma unroll
-          for (int v = 0; v < C::PPX / VV::CPV; ++v) {
-            reinterpret_cast<typename VV::T *>(P.out_T + gidx)[v] = VV::join(oT + v * VV::CPV);
-            if (MODE != M_LAP && MODE != M_S4)
-              reinterpret_cast<typename VV::T *>(P.out_acc + gidx)[v] = VV::join(oA + v * VV::CPV);
+          for (int v = 0; v < PPX / VV::CPV; ++v) {
+            st_stream(reinterpret_cast<typename VV::T *>(oTr) + v, VV::join(oT + v * VV::CPV));
+            if (MODE != M_LAP && MODE != M_S4) st_stream(reinterpret_cast<typename VV::T *>(oAr) + v, VV::join(oA + v * VV::CPV));
           }
         } else {
 #pragma unroll
-          for (int q = 0; q < C::PPX; ++q) {
+          for (int q = 0; q < PPX; ++q) {
             if (!valid[q]) continue;
-            P.out_T[gidx + q] = oT[q];
-            if (MODE != M_LAP && MODE != M_S4) P.out_acc[gidx + q] = oA[q];
+            oTr[q] = oT[q];
+            if (MODE != M_LAP && MODE != M_S4) oAr[q] = oA[q];
           }
         }
+        // queue shift: (k-2, k-1, k+1) <- (k-1, k, k+2)
+#pragma unroll
+        for (int q = 0; q < PPX; ++q) {
+          qm2[r][q] = qm1[r][q];
+          qm1[r][q] = run[q + 2];
+          qp1[r][q] = zp2[q];
+        }
       }
+      outT += P.plane;
+      if (MODE != M_LAP && MODE != M_S4) outA += P.plane;
+      __syncwarp();
       if (NPA) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&emptyP[pcnt % C::RP]);
-        ++pcnt;
+        if (lane == 0) mbar_arrive(&emptyP[sp]);
+        sp = inc(sp, RPM);
+        php ^= sp == 0;
       }
-      trelease(k - 2);
+      if (lane == 0) mbar_arrive(&emptyT[skm2]);  // plane k-2 is no longer read
+      skm2 = inc(skm2, RT);
+      sk = inc(sk, RT);
+      sk2 = inc(sk2, RT);
+      ph2 ^= sk2 == 0;
     }
-    for (int p = ke - 2; p < ke + 2; ++p) trelease(p);
+    pcnt += uint32_t(ke - kb) * (NPA ? 1 : 0);
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {  // planes ke-2 .. ke+1
+        mbar_arrive(&emptyT[skm2]);
+        skm2 = inc(skm2, RT);
+      }
+    }
     tcnt = tbase + uint32_t(ke - kb + 4);
   }
 }
