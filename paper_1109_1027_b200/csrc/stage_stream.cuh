@@ -37,28 +37,32 @@ enum Mode { M_S1 = 1, M_S2 = 2, M_S3 = 3, M_S4 = 4, M_LAP = 5 };
 // 2-3).  The pinned window of the T ring is planes k-2..k+2; the rest is prefetch, sized so
 // that each SM keeps ~100-200 KB of TMA loads in flight.
 template <int DIMS, typename R> struct Cfg;
-#ifndef NLSE_CFG3F
-#define NLSE_CFG3F 0
+// Ring depths from a shared-memory budget: the T ring keeps the pinned window (planes
+// k-1..k+2) plus a prefetch depth, the P ring gets the rest.
+template <int SLOT_B, int PT_B> struct Rings {
+  static constexpr int BUDGET = 210 * 1024;
+  static constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
+  static constexpr int mn(int a, int b) { return a < b ? a : b; }
+  static constexpr int RT0 = mn(24, BUDGET / SLOT_B);
+  static constexpr int RT1 = 4 + cdiv(40 * 1024, SLOT_B);
+  static constexpr int RP1 = mn(12, (BUDGET - RT1 * SLOT_B) / PT_B);
+  static constexpr int RT2 = 4 + cdiv(24 * 1024, SLOT_B);
+  static constexpr int RP2 = mn(8, (BUDGET - RT2 * SLOT_B) / (2 * PT_B));
+  static_assert(RT0 >= 5 && RP1 >= 2 && RP2 >= 2, "shared-memory budget too small for the tile");
+};
+// 3D tiles: 28 rows (y-halo overhead 32/28) handled by 14 consumer warps x 2 rows each;
+// chosen by a sweep over (TY, warps, rows/warp) on C4 (scripts/sweep.py).
+#ifndef NLSE3F_TY
+#define NLSE3F_TY 28
+#define NLSE3F_NCW 14
+#define NLSE3F_RPW 2
 #endif
-#if NLSE_CFG3F == 3
-template <> struct Cfg<3, float> {
-  static constexpr int TX = 64, TY = 24, PPX = 2, RPW = 1, NCW = 24, NBOX = 1, NBOXP = 1, W = 68;
-  static constexpr int RT0 = 13, RT1 = 8, RP1 = 6, RT2 = 7, RP2 = 3;
+template <> struct Cfg<3, float> : Rings<68 * (NLSE3F_TY + 4) * 8, 64 * NLSE3F_TY * 8> {
+  static constexpr int TX = 64, TY = NLSE3F_TY, PPX = 2, RPW = NLSE3F_RPW, NCW = NLSE3F_NCW, NBOX = 1, NBOXP = 1,
+                       W = 68;
 };
-#elif NLSE_CFG3F == 2
-template <> struct Cfg<3, float> {
-  static constexpr int TX = 64, TY = 16, PPX = 2, RPW = 2, NCW = 8, NBOX = 1, NBOXP = 1, W = 68;
-  static constexpr int RT0 = 18, RT1 = 10, RP1 = 10, RT2 = 9, RP2 = 5;
-};
-#else
-template <> struct Cfg<3, float> {
-  static constexpr int TX = 64, TY = 16, PPX = 2, RPW = 1, NCW = 16, NBOX = 1, NBOXP = 1, W = 68;
-  static constexpr int RT0 = 18, RT1 = 10, RP1 = 10, RT2 = 9, RP2 = 5;
-};
-#endif
-template <> struct Cfg<3, double> {
-  static constexpr int TX = 32, TY = 16, PPX = 1, RPW = 1, NCW = 16, NBOX = 1, NBOXP = 1, W = 36;
-  static constexpr int RT0 = 18, RT1 = 10, RP1 = 10, RT2 = 9, RP2 = 5;
+template <> struct Cfg<3, double> : Rings<36 * (28 + 4) * 16, 32 * 28 * 16> {
+  static constexpr int TX = 32, TY = 28, PPX = 1, RPW = 2, NCW = 14, NBOX = 1, NBOXP = 1, W = 36;
 };
 template <> struct Cfg<2, float> {
   static constexpr int TX = 512, TY = 1, PPX = 2, RPW = 1, NCW = 8, NBOX = 3, NBOXP = 2, W = 528;
@@ -339,7 +343,10 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
       centre(tslot(kb + 1), r, qp1[r]);
     }
     // running ring state: slots of planes k, k+2, k-2; parity of plane k+2; P ring
-    int sk = int((tbase + 2) % RT), sk2 = int((tbase + 4) % RT), skm2 = int(tbase % RT);
+    int sk = int((tbase + 2) % RT), sk2 = int((tbase + 4) % RT), skm1 = int((tbase + 1) % RT);
+    // plane kb-2 only seeded the queue: hand its slot back now
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&emptyT[tbase % RT]);
     uint32_t ph2 = ((tbase + 4) / RT) & 1;
     int sp = int(pcnt % RPM);
     uint32_t php = (pcnt / RPM) & 1;
@@ -359,9 +366,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
       const bool fast = inner_xy && zint && gz >= 2 && gz <= NZ - 3;  // no boundary point, no ghost
 
       if (!fast) {
-        const bool zg_lo = P.lo_face && k == 1;
-        const bool zg_hi = P.hi_face && k == nz - 2;
-        const bool do_ghost = (zint && (xlo || xhi || ylo || yhi)) || zg_lo || zg_hi;
+        const bool do_ghost = zint && (xlo || xhi || ylo || yhi);
         if (do_ghost) {
           // ---- ghost values (reading R8/R9, ghost form): one per face point that a depth-1
           // interior point of this tile/plane reads.
@@ -397,29 +402,16 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
               }
             }
           }
-          if (zg_lo || zg_hi) {
-            // streamed-axis face: ghost plane -1 (before output plane 1) or nz (before nz-2)
-            const int bz = zg_lo ? 0 : nz - 1, n = zg_lo ? 1 : -1;
-            CT *sb = tslot(bz), *si = tslot(bz + n), *sg = tslot(bz - n);
-            for (int task = ct; task < TX * TY; task += C::NCW * 32) {
-              const int lx = task % TX, ly = task / TX, gx = x0 + lx, gy = y0 + ly;
-              if (gx < 1 || gx > nx - 2) continue;
-              if (DIMS == 3 && (gy < 1 || gy > ny - 2)) continue;
-              CT cbv = at(sb, lx, ly), cin = at(si, lx, ly);
-              CT D = lambda_b(P, cbv, potential(P, gx, gy, bz));
-              D = D - d2(at(sb, lx - 1, ly), cbv, at(sb, lx + 1, ly), P.ihx2);
-              if (DIMS == 3) D = D - d2(at(sb, lx, ly - 1), cbv, at(sb, lx, ly + 1), P.ihy2);
-              at(sg, lx, ly) = axpy(R(2) * cbv - cin, P.hz2, D);
-            }
-          }
           fence_proxy_async_smem();  // generic writes to slots precede later TMA refills
           named_bar_sync(1, C::NCW * 32);
-          if (zg_lo) {
-#pragma unroll
-            for (int r = 0; r < RPW; ++r) centre(tslot(-1), r, qm2[r]);
-          }
         }
       }
+      // streamed-axis faces: the ghost plane -1 (read as plane k-2 at k = 1) and the ghost
+      // plane nz (read as plane k+2 at k = nz-2) are formed per thread, in registers, from
+      // the face plane (queue + its slot, for the tangential differences) and the first
+      // interior plane.
+      const bool zg_lo = !fast && P.lo_face && k == 1;
+      const bool zg_hi = !fast && P.hi_face && k == nz - 2;
 
       // ---- stencil + RHS + stage combine for this thread's points of plane k
       const CT *s0 = ring + size_t(sk) * LY::SLOT + toff, *sp2 = ring + size_t(sk2) * LY::SLOT + toff;
@@ -430,6 +422,24 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
         lds_run<R, PPX + 4>(s0 + r * W, run);
         CT zp2[PPX];
         lds_run<R, PPX>(sp2 + r * W + 2, zp2);
+        if (zg_lo || zg_hi) {
+          // face plane b = 0 (lo) or nz-1 (hi): its values are qm1 (lo) or qp1 (hi); the first
+          // interior plane is the centre k; tangential neighbours come from b's slot
+          const CT *sb = ring + size_t(zg_lo ? (sk == 0 ? RT - 1 : sk - 1) : (sk + 1 == RT ? 0 : sk + 1)) * LY::SLOT + toff;
+#pragma unroll
+          for (int q = 0; q < PPX; ++q) {
+            const int gx = x0 + lx0 + q;
+            if (gx < 1 || gx > nx - 2 || (DIMS == 3 && (gy < 1 || gy > ny - 2))) continue;
+            const CT cbv = zg_lo ? qm1[r][q] : qp1[r][q];
+            const CT *pb = sb + r * W + 2 + q;
+            CT D = lambda_b(P, cbv, potential(P, gx, gy, zg_lo ? 0 : nz - 1));
+            D = D - d2(pb[-1], cbv, pb[1], P.ihx2);
+            if (DIMS == 3) D = D - d2(pb[-W], cbv, pb[W], P.ihy2);
+            const CT g = axpy(R(2) * cbv - run[q + 2], P.hz2, D);
+            if (zg_lo) qm2[r][q] = g;
+            else zp2[q] = g;
+          }
+        }
         CT ym2[PPX], ym1[PPX], yp1[PPX], yp2[PPX];
         if (DIMS == 3) {
           lds_run<R, PPX>(s0 + (r - 2) * W + 2, ym2);
@@ -520,8 +530,8 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
         sp = inc(sp, RPM);
         php ^= sp == 0;
       }
-      if (lane == 0) mbar_arrive(&emptyT[skm2]);  // plane k-2 is no longer read
-      skm2 = inc(skm2, RT);
+      if (lane == 0) mbar_arrive(&emptyT[skm1]);  // plane k-1 is no longer read
+      skm1 = inc(skm1, RT);
       sk = inc(sk, RT);
       sk2 = inc(sk2, RT);
       ph2 ^= sk2 == 0;
@@ -530,9 +540,9 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
     __syncwarp();
     if (lane == 0) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {  // planes ke-2 .. ke+1
-        mbar_arrive(&emptyT[skm2]);
-        skm2 = inc(skm2, RT);
+      for (int i = 0; i < 3; ++i) {  // planes ke-1 .. ke+1
+        mbar_arrive(&emptyT[skm1]);
+        skm1 = inc(skm1, RT);
       }
     }
     tcnt = tbase + uint32_t(ke - kb + 4);
