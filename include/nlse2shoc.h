@@ -101,6 +101,15 @@ nlse2shoc_status nlse2shoc_get_unique_id(void *id128);
 nlse2shoc_status nlse2shoc_create_sharded(nlse2shoc_t *out, int dims, const int64_t N[3], const double h[3],
                                           double a, double s, const nlse2shoc_potential *V, nlse2shoc_bc bc,
                                           nlse2shoc_dtype dtype, const void *id128, int rank, int nranks);
+/* Single-GPU emulation of the z-slab sharding (2D/3D): one handle holding nslabs virtual
+ * slabs, split exactly like nlse2shoc_split, that exchange their 2-plane halos by
+ * device-to-device copies instead of NCCL and run the same kernels as real shards.  The
+ * caller's Psi / L are the WHOLE grid.  Results are bitwise identical to a single-slab
+ * handle (no reduction in the step; halos are exact copies); used to test the sharded
+ * path where only one GPU is available.  EINVAL for dims = 1 or nslabs < 1.            */
+nlse2shoc_status nlse2shoc_create_loopback(nlse2shoc_t *out, int dims, const int64_t N[3], const double h[3],
+                                           double a, double s, const nlse2shoc_potential *V, nlse2shoc_bc bc,
+                                           nlse2shoc_dtype dtype, int nslabs);
 /* Slab owned by this handle along the slowest axis (z in 3D, y in 2D, whole grid in 1D). */
 nlse2shoc_status nlse2shoc_local_extent(nlse2shoc_t, int64_t *z0, int64_t *nz);
 /* Split rule used by create_sharded (pure host function, no handle needed). */

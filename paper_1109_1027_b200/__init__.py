@@ -14,7 +14,7 @@ from ._lib import BC, DTYPE, VKIND, NLSE2SHOCError, Potential, check, lib
 __all__ = [
     "Solver", "NLSE2SHOCError", "nlse2shoc_create", "nlse2shoc_create_sharded", "nlse2shoc_get_unique_id",
     "nlse2shoc_laplacian", "nlse2shoc_rk4", "nlse2shoc_stability_bound", "nlse2shoc_check_finite",
-    "nlse2shoc_split", "nlse2shoc_version", "solver_from_work",
+    "nlse2shoc_split", "nlse2shoc_version", "solver_from_work", "nlse2shoc_create_loopback",
 ]
 
 
@@ -90,6 +90,15 @@ def nlse2shoc_create_sharded(dims, N, h, a, s, V, bc, dtype, uid: bytes, rank: i
     return H, keep
 
 
+def nlse2shoc_create_loopback(dims, N, h, a, s, V, bc, dtype, nslabs: int):
+    H = ctypes.c_void_p()
+    n, hh = _args(dims, N, h)
+    pv, keep = _potential(V, dims)
+    check(lib().nlse2shoc_create_loopback(ctypes.byref(H), int(dims), n, hh, float(a), float(s), ctypes.byref(pv),
+                                          BC[bc], DTYPE[dtype], int(nslabs)), "create_loopback")
+    return H, keep
+
+
 def nlse2shoc_laplacian(H, psi, L, stream=None):
     check(lib().nlse2shoc_laplacian(H, _ptr(psi), _ptr(L), _stream(stream)), "laplacian")
     return L
@@ -119,6 +128,8 @@ class Solver:
         self.N = [int(v) for v in list(N)[:dims]]
         if shard is None:
             self._h, self._keep = nlse2shoc_create(dims, N, h, a, s, V, bc, dtype)
+        elif "loopback" in shard:
+            self._h, self._keep = nlse2shoc_create_loopback(dims, N, h, a, s, V, bc, dtype, shard["loopback"])
         else:
             self._h, self._keep = nlse2shoc_create_sharded(dims, N, h, a, s, V, bc, dtype, shard["uid"],
                                                            shard["rank"], shard["nranks"])

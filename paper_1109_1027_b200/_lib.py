@@ -56,6 +56,9 @@ def lib():
             "nlse2shoc_create_sharded": [ctypes.POINTER(H), ctypes.c_int, i643, dbl3, ctypes.c_double, ctypes.c_double,
                                          ctypes.POINTER(Potential), ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
                                          ctypes.c_int, ctypes.c_int],
+            "nlse2shoc_create_loopback": [ctypes.POINTER(H), ctypes.c_int, i643, dbl3, ctypes.c_double,
+                                          ctypes.c_double, ctypes.POINTER(Potential), ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_int],
             "nlse2shoc_local_extent": [H, i64p, i64p],
             "nlse2shoc_split": [ctypes.c_int64, ctypes.c_int, ctypes.c_int, i64p, i64p],
             "nlse2shoc_set_variant": [H, ctypes.c_int],
@@ -94,7 +97,8 @@ def check(status, where):
 
 # Header symbols, for the "library exports everything include/*.h declares" test.
 EXPORTS = [
-    "nlse2shoc_create", "nlse2shoc_get_unique_id", "nlse2shoc_create_sharded", "nlse2shoc_local_extent",
+    "nlse2shoc_create", "nlse2shoc_get_unique_id", "nlse2shoc_create_sharded", "nlse2shoc_create_loopback",
+    "nlse2shoc_local_extent",
     "nlse2shoc_split", "nlse2shoc_workspace_bytes", "nlse2shoc_set_variant", "nlse2shoc_laplacian",
     "nlse2shoc_rk4", "nlse2shoc_stability_bound", "nlse2shoc_check_finite", "nlse2shoc_last_launch_count",
     "nlse2shoc_strerror", "nlse2shoc_last_error", "nlse2shoc_version", "nlse2shoc_destroy",

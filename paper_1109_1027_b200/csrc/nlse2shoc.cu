@@ -68,7 +68,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 struct Field {  // one pitched field of the local slab (+ its two halo buffers when sharded)
   void *ptr = nullptr;
   void *halo_lo = nullptr, *halo_hi = nullptr;
-  CUtensorMap tm{}, tm_lo{}, tm_hi{};
+  CUtensorMap tm{}, tm_lo{}, tm_hi{};  // stencil-input boxes (tile + halo) over the slab / halos
+  CUtensorMap tm_pt{};                 // pointwise tile boxes (Psi^n, acc reads)
 };
 
 struct nlse2shoc_s {
@@ -95,6 +96,11 @@ struct nlse2shoc_s {
   size_t bytes = 0;
   int num_sms = 148;
   int64_t launches = 0;
+  // loopback (single-GPU emulation of z-slab sharding, SURVEY §4 T3'): virtual slabs that
+  // exchange halos by device copies instead of NCCL; empty for ordinary handles
+  std::vector<nlse2shoc_s *> slabs;
+  bool loop_member = false;
+  void *Lw = nullptr;  // pitched staging for the Laplacian output (odd-N_x complex64 only)
 #ifdef NLSE_WITH_NCCL
   ncclComm_t comm = nullptr;
 #endif
@@ -289,93 +295,99 @@ static nlse2shoc_status launch_two(int, int stage, const cplx<R> *in, const cplx
 }
 
 // ----------------------------------------------------------------------- stage drivers
-// Fused RK4: stage s reads X_{s-1} (stencil) and writes the next stage input + acc.
+// Stage s = 1..4 of an RK4 step reads X_{s-1} as its stencil input (X_0 = Psi^n) and writes
+// the next stage input and the accumulator (Psi-space form):
+//   1: acc = Psi + k/6 K1,  T_A = Psi + k/2 K1        3: acc += k/3 K3,  T_A = Psi + k K3
+//   2: acc += k/3 K2,       T_B = Psi + k/2 K2        4: Psi = acc + k/6 K4
+// s = 5 is the Laplacian (Psi -> L).
+static Field &stage_input(nlse2shoc_t H, Field &psi, int s) { return (s == 1 || s == 5) ? psi : (s == 3 ? H->TB : H->TA); }
+
+template <int DIMS, typename R, int MODE>
+static nlse2shoc_status launch_mode(nlse2shoc_t H, Field &psi, Field &in, StageParams<R> &P, cudaStream_t st) {
+  if (H->variant == 1) {
+    TwoParams<R> Q;
+    two_params<R>(H->dims, H->h, Q);
+    return launch_two<DIMS, R>(0, MODE, reinterpret_cast<const cplx<R> *>(in.ptr),
+                               reinterpret_cast<const cplx<R> *>(in.halo_lo), reinterpret_cast<const cplx<R> *>(in.halo_hi),
+                               reinterpret_cast<const cplx<R> *>(psi.ptr), reinterpret_cast<const cplx<R> *>(H->acc.ptr),
+                               reinterpret_cast<cplx<R> *>(H->D.ptr), P, Q, st, H->launches);
+  }
+  if constexpr (DIMS == 1) return launch_line<R, MODE>(H, in.ptr, psi.ptr, H->acc.ptr, P, st);
+  else return launch_stream<DIMS, R, MODE>(H, in, &psi.tm_pt, &H->acc.tm_pt, P, st);
+}
+
 template <int DIMS, typename R>
-static nlse2shoc_status rk4_fused(nlse2shoc_t H, Field &psi, double dt, int64_t nsteps, cudaStream_t st) {
+static nlse2shoc_status launch_stage(nlse2shoc_t H, Field &psi, int s, double dt, void *L, cudaStream_t st) {
   StageParams<R> P;
   fill_params<R>(H, P);
+  Field &in = stage_input(H, psi, s);
   cplx<R> *pPsi = reinterpret_cast<cplx<R> *>(psi.ptr), *pA = reinterpret_cast<cplx<R> *>(H->TA.ptr),
           *pB = reinterpret_cast<cplx<R> *>(H->TB.ptr), *pAcc = reinterpret_cast<cplx<R> *>(H->acc.ptr);
-  CUtensorMap tm_psi{}, tm_acc{};
-  if constexpr (DIMS >= 2) {
-    TRY((Maps<DIMS, R>::point(H, &tm_psi, psi.ptr)));
-    TRY((Maps<DIMS, R>::point(H, &tm_acc, H->acc.ptr)));
+  switch (s) {
+    case 1:
+      P.ca = R(dt / 6.0); P.cb = R(dt / 2.0); P.out_T = pA; P.out_acc = pAcc;
+      return launch_mode<DIMS, R, M_S1>(H, psi, in, P, st);
+    case 2:
+      P.ca = R(dt / 3.0); P.cb = R(dt / 2.0); P.out_T = pB; P.out_acc = pAcc;
+      return launch_mode<DIMS, R, M_S2>(H, psi, in, P, st);
+    case 3:
+      P.ca = R(dt / 3.0); P.cb = R(dt); P.out_T = pA; P.out_acc = pAcc;
+      return launch_mode<DIMS, R, M_S3>(H, psi, in, P, st);
+    case 4:
+      P.ca = R(0); P.cb = R(dt / 6.0); P.out_T = pPsi; P.out_acc = nullptr;
+      return launch_mode<DIMS, R, M_S4>(H, psi, in, P, st);
+    default:
+      P.out_T = reinterpret_cast<cplx<R> *>(L);
+      return launch_mode<DIMS, R, M_LAP>(H, psi, in, P, st);
   }
-  const R k = R(dt);
-  for (int64_t n = 0; n < nsteps; ++n) {
-    // stage 1: K1 = F(Psi^n); acc = Psi^n + k/6 K1; T_A = Psi^n + k/2 K1
-    TRY(halo_exchange(H, psi, st));
-    P.ca = R(dt / 6.0); P.cb = R(dt / 2.0); P.out_T = pA; P.out_acc = pAcc;
-    if constexpr (DIMS == 1) TRY((launch_line<R, M_S1>(H, pPsi, pPsi, pAcc, P, st)));
-    else TRY((launch_stream<DIMS, R, M_S1>(H, psi, nullptr, nullptr, P, st)));
-    // stage 2: K2 = F(T_A); acc += k/3 K2; T_B = Psi^n + k/2 K2
-    TRY(halo_exchange(H, H->TA, st));
-    P.ca = R(dt / 3.0); P.cb = R(dt / 2.0); P.out_T = pB; P.out_acc = pAcc;
-    if constexpr (DIMS == 1) TRY((launch_line<R, M_S2>(H, pA, pPsi, pAcc, P, st)));
-    else TRY((launch_stream<DIMS, R, M_S2>(H, H->TA, &tm_psi, &tm_acc, P, st)));
-    // stage 3: K3 = F(T_B); acc += k/3 K3; T_A = Psi^n + k K3
-    TRY(halo_exchange(H, H->TB, st));
-    P.ca = R(dt / 3.0); P.cb = k; P.out_T = pA; P.out_acc = pAcc;
-    if constexpr (DIMS == 1) TRY((launch_line<R, M_S3>(H, pB, pPsi, pAcc, P, st)));
-    else TRY((launch_stream<DIMS, R, M_S3>(H, H->TB, &tm_psi, &tm_acc, P, st)));
-    // stage 4: K4 = F(T_A); Psi^{n+1} = acc + k/6 K4 (pointwise, in place over Psi^n)
-    TRY(halo_exchange(H, H->TA, st));
-    P.ca = R(0); P.cb = R(dt / 6.0); P.out_T = pPsi; P.out_acc = nullptr;
-    if constexpr (DIMS == 1) TRY((launch_line<R, M_S4>(H, pA, pPsi, pAcc, P, st)));
-    else TRY((launch_stream<DIMS, R, M_S4>(H, H->TA, nullptr, &tm_acc, P, st)));
-  }
-  return NLSE2SHOC_OK;
 }
 
-template <int DIMS, typename R> static nlse2shoc_status lap_fused(nlse2shoc_t H, Field &psi, void *L, cudaStream_t st) {
-  StageParams<R> P;
-  fill_params<R>(H, P);
-  P.out_T = reinterpret_cast<cplx<R> *>(L);
-  TRY(halo_exchange(H, psi, st));
-  if constexpr (DIMS == 1) return launch_line<R, M_LAP>(H, psi.ptr, psi.ptr, psi.ptr, P, st);
-  else return launch_stream<DIMS, R, M_LAP>(H, psi, nullptr, nullptr, P, st);
+static nlse2shoc_status stage(nlse2shoc_t H, Field &psi, int s, double dt, void *L, cudaStream_t st) {
+  const bool f32 = H->dtype == NLSE2SHOC_C64;
+  switch (H->dims) {
+    case 1: return f32 ? launch_stage<1, float>(H, psi, s, dt, L, st) : launch_stage<1, double>(H, psi, s, dt, L, st);
+    case 2: return f32 ? launch_stage<2, float>(H, psi, s, dt, L, st) : launch_stage<2, double>(H, psi, s, dt, L, st);
+    default: return f32 ? launch_stage<3, float>(H, psi, s, dt, L, st) : launch_stage<3, double>(H, psi, s, dt, L, st);
+  }
 }
 
-// Two-kernel (single-storage D in HBM, PAPER.md `2d2shocs1/2`, `3d2shocs`) RK4.
-template <int DIMS, typename R>
-static nlse2shoc_status rk4_two(nlse2shoc_t H, Field &psi, double dt, int64_t nsteps, cudaStream_t st) {
-  StageParams<R> P;
-  fill_params<R>(H, P);
-  TwoParams<R> Q;
-  two_params<R>(H->dims, H->h, Q);
-  cplx<R> *pPsi = reinterpret_cast<cplx<R> *>(psi.ptr), *pA = reinterpret_cast<cplx<R> *>(H->TA.ptr),
-          *pB = reinterpret_cast<cplx<R> *>(H->TB.ptr), *pAcc = reinterpret_cast<cplx<R> *>(H->acc.ptr),
-          *pD = reinterpret_cast<cplx<R> *>(H->D.ptr);
-  Field *ins[4] = {&psi, &H->TA, &H->TB, &H->TA};
-  cplx<R> *outs[4] = {pA, pB, pA, pPsi};
-  const double ca[4] = {dt / 6.0, dt / 3.0, dt / 3.0, 0.0}, cb[4] = {dt / 2.0, dt / 2.0, dt, dt / 6.0};
-  for (int64_t n = 0; n < nsteps; ++n) {
-    for (int s = 0; s < 4; ++s) {
-      TRY(halo_exchange(H, *ins[s], st));
-      P.ca = R(ca[s]);
-      P.cb = R(cb[s]);
-      P.out_T = outs[s];
-      P.out_acc = s < 3 ? pAcc : nullptr;
-      const cplx<R> *in = reinterpret_cast<const cplx<R> *>(ins[s]->ptr);
-      const cplx<R> *lo = reinterpret_cast<const cplx<R> *>(ins[s]->halo_lo);
-      const cplx<R> *hi = reinterpret_cast<const cplx<R> *>(ins[s]->halo_hi);
-      TRY((launch_two<DIMS, R>(H->num_sms, s + 1, in, lo, hi, pPsi, pAcc, pD, P, Q, st, H->launches)));
+// A "view" is the list of slabs a call works on: one handle (single GPU, or this rank's
+// slab under NCCL sharding), or the virtual slabs of a loopback handle.
+struct View {
+  std::vector<nlse2shoc_t> hs;
+  std::vector<Field> psis;
+};
+
+// Halo exchange of stage s's stencil input (2 planes per side): NCCL for a real shard,
+// device-to-device copies between the virtual slabs of a loopback handle.
+static nlse2shoc_status exchange(View &v, int s, cudaStream_t st) {
+  const size_t P = v.hs.size();
+  if (P == 1) return halo_exchange(v.hs[0], stage_input(v.hs[0], v.psis[0], s), st);
+  for (size_t i = 0; i < P; ++i) {
+    nlse2shoc_t H = v.hs[i];
+    Field &f = stage_input(H, v.psis[i], s);
+    const size_t b2 = size_t(2 * H->plane) * H->S;
+    if (i > 0) {
+      nlse2shoc_t Hn = v.hs[i - 1];
+      Field &g = stage_input(Hn, v.psis[i - 1], s);
+      CUDA_TRY(cudaMemcpyAsync(f.halo_lo, reinterpret_cast<char *>(g.ptr) + size_t(Hn->nz - 2) * Hn->plane * Hn->S, b2,
+                               cudaMemcpyDeviceToDevice, st));
+    }
+    if (i + 1 < P) {
+      Field &g = stage_input(v.hs[i + 1], v.psis[i + 1], s);
+      CUDA_TRY(cudaMemcpyAsync(f.halo_hi, g.ptr, b2, cudaMemcpyDeviceToDevice, st));
     }
   }
   return NLSE2SHOC_OK;
 }
 
-template <int DIMS, typename R> static nlse2shoc_status lap_two(nlse2shoc_t H, Field &psi, void *L, cudaStream_t st) {
-  StageParams<R> P;
-  fill_params<R>(H, P);
-  TwoParams<R> Q;
-  two_params<R>(H->dims, H->h, Q);
-  P.out_T = reinterpret_cast<cplx<R> *>(L);
-  TRY(halo_exchange(H, psi, st));
-  const cplx<R> *in = reinterpret_cast<const cplx<R> *>(psi.ptr);
-  return launch_two<DIMS, R>(H->num_sms, 5, in, reinterpret_cast<const cplx<R> *>(psi.halo_lo),
-                             reinterpret_cast<const cplx<R> *>(psi.halo_hi), nullptr, nullptr,
-                             reinterpret_cast<cplx<R> *>(H->D.ptr), P, Q, st, H->launches);
+static nlse2shoc_status run_rk4(View &v, double dt, int64_t nsteps, cudaStream_t st) {
+  for (int64_t n = 0; n < nsteps; ++n)
+    for (int s = 1; s <= 4; ++s) {
+      TRY(exchange(v, s, st));
+      for (size_t i = 0; i < v.hs.size(); ++i) TRY(stage(v.hs[i], v.psis[i], s, dt, nullptr, st));
+    }
+  return NLSE2SHOC_OK;
 }
 
 // ------------------------------------------------------------------------------ create
@@ -396,10 +408,12 @@ static nlse2shoc_status alloc_field(nlse2shoc_t H, Field &f, bool halos) {
 
 template <typename R> static nlse2shoc_status encode_field_maps(nlse2shoc_t H, Field &f) {
   if (H->dims == 3) {
+    TRY((Maps<3, R>::point(H, &f.tm_pt, f.ptr)));
     TRY((Maps<3, R>::stencil(H, &f.tm, f.ptr, H->nz)));
     if (f.halo_lo) TRY((Maps<3, R>::stencil(H, &f.tm_lo, f.halo_lo, 2)));
     if (f.halo_hi) TRY((Maps<3, R>::stencil(H, &f.tm_hi, f.halo_hi, 2)));
   } else if (H->dims == 2) {
+    TRY((Maps<2, R>::point(H, &f.tm_pt, f.ptr)));
     TRY((Maps<2, R>::stencil(H, &f.tm, f.ptr, H->nz)));
     if (f.halo_lo) TRY((Maps<2, R>::stencil(H, &f.tm_lo, f.halo_lo, 2)));
     if (f.halo_hi) TRY((Maps<2, R>::stencil(H, &f.tm_hi, f.halo_hi, 2)));
@@ -433,7 +447,9 @@ template <typename R> static void build_tables(nlse2shoc_t H, std::vector<unsign
 
 static nlse2shoc_status create_impl(nlse2shoc_t *out, int dims, const int64_t N[3], const double h[3], double a,
                                     double s, const nlse2shoc_potential *V, nlse2shoc_bc bc, nlse2shoc_dtype dtype,
-                                    int rank, int nranks, const void *id128) {
+                                    int rank, int nranks, const void *id128, int loop = 0) {
+  // loop > 0: this is virtual slab `rank` of a loopback handle (sharded layout, no NCCL);
+  // loop < 0: the loopback parent of -loop virtual slabs (owns only the staging buffers)
   if (!out) return fail(NLSE2SHOC_EINVAL, "out is NULL");
   *out = nullptr;
   if (dims < 1 || dims > 3) return fail(NLSE2SHOC_EINVAL, "dims must be 1, 2 or 3");
@@ -462,9 +478,9 @@ static nlse2shoc_status create_impl(nlse2shoc_t *out, int dims, const int64_t N[
       if (!std::isfinite(pv.w[d]) || !std::isfinite(pv.c[d]) || !std::isfinite(pv.xmin[d]))
         return fail(NLSE2SHOC_EINVAL, "non-finite harmonic parameters");
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(NLSE2SHOC_EINVAL, "bad rank / nranks");
-  if (nranks > 1 && dims == 1) return fail(NLSE2SHOC_EINVAL, "1D grids are not sharded (replicas only)");
+  if ((nranks > 1 || loop != 0) && dims == 1) return fail(NLSE2SHOC_EINVAL, "1D grids are not sharded (replicas only)");
 #ifndef NLSE_WITH_NCCL
-  if (nranks > 1) return fail(NLSE2SHOC_EUNSUPPORTED, "built without NCCL");
+  if (nranks > 1 && loop == 0) return fail(NLSE2SHOC_EUNSUPPORTED, "built without NCCL");
 #endif
 
   auto *H = new nlse2shoc_s();
@@ -478,7 +494,8 @@ static nlse2shoc_status create_impl(nlse2shoc_t *out, int dims, const int64_t N[
   H->S = dtype == NLSE2SHOC_C64 ? 8 : 16;
   H->rank = rank;
   H->nranks = nranks;
-  H->sharded = id128 != nullptr;
+  H->sharded = id128 != nullptr || loop > 0;
+  H->loop_member = loop > 0;
   cudaGetDevice(&H->device);
   cudaDeviceGetAttribute(&H->num_sms, cudaDevAttrMultiProcessorCount, H->device);
   H->NZ = dims >= 2 ? N[dims - 1] : 1;
@@ -489,6 +506,9 @@ static nlse2shoc_status create_impl(nlse2shoc_t *out, int dims, const int64_t N[
   if (dims >= 2 && nz < 2) { delete H; return fail(NLSE2SHOC_EINVAL, "each slab needs >= 2 planes"); }
   H->z0 = z0;
   H->nz = dims >= 2 ? nz : 1;
+  if (loop > 0 && pv.kind == NLSE2SHOC_V_ARRAY)  // virtual slab: its part of the whole-grid V
+    H->V.data = reinterpret_cast<const char *>(pv.data) + size_t(z0) * size_t(N[0]) * size_t(dims == 3 ? N[1] : 1) *
+                                                        (dtype == NLSE2SHOC_C64 ? sizeof(float) : sizeof(double));
   if (dims == 1) H->nz = 1;
   const int64_t cpv = 16 / int64_t(H->S);
   H->pitch = dims == 1 ? H->nx : ((H->nx + cpv - 1) / cpv) * cpv;
@@ -498,11 +518,35 @@ static nlse2shoc_status create_impl(nlse2shoc_t *out, int dims, const int64_t N[
 
   nlse2shoc_status st = NLSE2SHOC_OK;
   auto chk = [&](nlse2shoc_status r) { if (st == NLSE2SHOC_OK) st = r; };
+  if (loop < 0) {  // loopback parent: virtual slabs + staging buffers only
+    const int P = -loop;
+    for (int i = 0; i < P && st == NLSE2SHOC_OK; ++i) {
+      nlse2shoc_t S = nullptr;
+      chk(create_impl(&S, dims, N, h, a, s, V, bc, dtype, i, P, nullptr, 1));
+      if (S) H->slabs.push_back(S);
+    }
+    if (st == NLSE2SHOC_OK && H->pitch != H->nx) {
+      chk(alloc_field(H, H->psiw, false));
+      if (st == NLSE2SHOC_OK && cudaMalloc(&H->Lw, size_t(H->local_elems) * H->S) != cudaSuccess)
+        chk(fail(NLSE2SHOC_ENOMEM, "staging allocation failed"));
+    }
+    if (st != NLSE2SHOC_OK) {
+      std::string keep = g_last_error;
+      nlse2shoc_destroy(H);
+      *out = nullptr;
+      g_last_error = keep;
+    }
+    return st;
+  }
   chk(alloc_field(H, H->TA, true));
   chk(alloc_field(H, H->TB, true));
   chk(alloc_field(H, H->acc, false));
-  if (st == NLSE2SHOC_OK && H->pitch != H->nx) chk(alloc_field(H, H->psiw, true));
-  if (st == NLSE2SHOC_OK && H->sharded && H->pitch == H->nx) {
+  if (st == NLSE2SHOC_OK && H->pitch != H->nx && !H->loop_member) {
+    chk(alloc_field(H, H->psiw, true));
+    if (st == NLSE2SHOC_OK && cudaMalloc(&H->Lw, size_t(H->local_elems) * H->S) != cudaSuccess)
+      chk(fail(NLSE2SHOC_ENOMEM, "staging allocation failed"));
+  }
+  if (st == NLSE2SHOC_OK && H->sharded && (H->pitch == H->nx || H->loop_member)) {
     // halo buffers for the caller's Psi (zero-copy path)
     const size_t hb = size_t(2 * H->plane) * H->S;
     if (cudaMalloc(&H->psiw.halo_lo, hb) != cudaSuccess || cudaMalloc(&H->psiw.halo_hi, hb) != cudaSuccess)
@@ -512,6 +556,7 @@ static nlse2shoc_status create_impl(nlse2shoc_t *out, int dims, const int64_t N[
   if (st == NLSE2SHOC_OK) {
     chk(encode_maps(H, H->TA));
     chk(encode_maps(H, H->TB));
+    chk(encode_maps(H, H->acc));
     if (H->psiw.ptr) chk(encode_maps(H, H->psiw));
   }
   if (st == NLSE2SHOC_OK && pv.kind == NLSE2SHOC_V_HARMONIC) {
@@ -529,7 +574,7 @@ static nlse2shoc_status create_impl(nlse2shoc_t *out, int dims, const int64_t N[
       chk(fail(NLSE2SHOC_ENOMEM, "reduction buffer allocation failed"));
   }
 #ifdef NLSE_WITH_NCCL
-  if (st == NLSE2SHOC_OK && H->sharded) {
+  if (st == NLSE2SHOC_OK && H->sharded && id128) {
     ncclUniqueId id;
     std::memcpy(&id, id128, sizeof(id));
     ncclResult_t r = ncclCommInitRank(&H->comm, nranks, id, rank);
@@ -550,33 +595,60 @@ static nlse2shoc_status create_impl(nlse2shoc_t *out, int dims, const int64_t N[
 }
 
 // --------------------------------------------------------------------------- psi views
-// Wrap the caller's psi as the working Field (zero-copy) or stage it through the pitched
-// copy (only complex64 with odd N_x in 2D/3D, where rows are not 16-byte multiples).
-static nlse2shoc_status psi_in(nlse2shoc_t H, void *psi, Field &w, cudaStream_t st) {
-  if (H->pitch == H->nx) {
-    w.ptr = psi;
-    w.halo_lo = H->psiw.halo_lo;
-    w.halo_hi = H->psiw.halo_hi;
-    if (H->dims >= 2) {
-      if (H->dtype == NLSE2SHOC_C64) {
-        TRY(encode_field_maps<float>(H, w));
-      } else {
-        TRY(encode_field_maps<double>(H, w));
-      }
+// The caller's Psi is used in place (zero-copy) when its rows are whole 16-byte vectors;
+// otherwise (complex64 with odd N_x in 2D/3D) it is staged through a pitched copy.
+static nlse2shoc_status wrap_psi(nlse2shoc_t S, void *base, Field &w) {
+  w = Field();
+  w.ptr = base;
+  w.halo_lo = S->psiw.halo_lo;
+  w.halo_hi = S->psiw.halo_hi;
+  if (S->dims >= 2) {
+    if (S->dtype == NLSE2SHOC_C64) {
+      TRY(encode_field_maps<float>(S, w));
+    } else {
+      TRY(encode_field_maps<double>(S, w));
     }
+  }
+  return NLSE2SHOC_OK;
+}
+
+// Build the view of a call on psi (caller layout).  *work receives the pitched base the
+// kernels use (== psi on the zero-copy path).
+static nlse2shoc_status make_view(nlse2shoc_t H, void *psi, View &v, void **work, cudaStream_t st) {
+  void *base = psi;
+  if (H->pitch != H->nx) {
+    base = H->psiw.ptr;
+    CUDA_TRY(cudaMemcpy2DAsync(base, H->pitch * H->S, psi, H->nx * H->S, H->nx * H->S, H->ny * H->nz,
+                               cudaMemcpyDeviceToDevice, st));
+  }
+  *work = base;
+  v.hs.clear();
+  v.psis.clear();
+  if (H->slabs.empty()) {
+    v.hs.push_back(H);
+    v.psis.emplace_back();
+    if (base == H->psiw.ptr) v.psis.back() = H->psiw;
+    else TRY(wrap_psi(H, base, v.psis.back()));
     return NLSE2SHOC_OK;
   }
-  w = H->psiw;
-  CUDA_TRY(cudaMemcpy2DAsync(w.ptr, H->pitch * H->S, psi, H->nx * H->S, H->nx * H->S, H->ny * H->nz,
+  for (nlse2shoc_t S : H->slabs) {
+    v.hs.push_back(S);
+    v.psis.emplace_back();
+    TRY(wrap_psi(S, reinterpret_cast<char *>(base) + size_t(S->z0) * S->plane * S->S, v.psis.back()));
+  }
+  return NLSE2SHOC_OK;
+}
+
+static nlse2shoc_status unstage(nlse2shoc_t H, void *dst, const void *work, cudaStream_t st) {
+  if (work == dst) return NLSE2SHOC_OK;
+  CUDA_TRY(cudaMemcpy2DAsync(dst, H->nx * H->S, work, H->pitch * H->S, H->nx * H->S, H->ny * H->nz,
                              cudaMemcpyDeviceToDevice, st));
   return NLSE2SHOC_OK;
 }
 
-static nlse2shoc_status psi_out(nlse2shoc_t H, void *psi, const void *src, cudaStream_t st) {
-  if (src == psi) return NLSE2SHOC_OK;
-  CUDA_TRY(cudaMemcpy2DAsync(psi, H->nx * H->S, src, H->pitch * H->S, H->nx * H->S, H->ny * H->nz,
-                             cudaMemcpyDeviceToDevice, st));
-  return NLSE2SHOC_OK;
+static void reset_launches(nlse2shoc_t H) {
+  H->launches = 0;
+  for (nlse2shoc_t S : H->slabs) S->launches = 0;
 }
 
 static nlse2shoc_status check_ptr(const void *p, const char *name) {
@@ -595,6 +667,19 @@ static nlse2shoc_status ensure_D(nlse2shoc_t H) {
 }
 
 template <typename R> static nlse2shoc_status reduce_N(nlse2shoc_t H, const void *psi, double out[3], cudaStream_t st) {
+  if (!H->slabs.empty()) {  // loopback: fold the virtual slabs
+    out[0] = INFINITY;
+    out[1] = -INFINITY;
+    out[2] = 0;
+    for (nlse2shoc_t S : H->slabs) {
+      double r[3];
+      TRY(reduce_N<R>(S, reinterpret_cast<const char *>(psi) + size_t(S->z0) * S->nx * S->ny * S->S, r, st));
+      out[0] = std::min(out[0], r[0]);
+      out[1] = std::max(out[1], r[1]);
+      out[2] += r[2];
+    }
+    return NLSE2SHOC_OK;
+  }
   StageParams<R> P;
   fill_params<R>(H, P);
   P.pitch = H->nx;  // caller layout
@@ -614,7 +699,7 @@ template <typename R> static nlse2shoc_status reduce_N(nlse2shoc_t H, const void
     out[2] += part[3 * b + 2];
   }
 #ifdef NLSE_WITH_NCCL
-  if (H->sharded && H->nranks > 1) {
+  if (H->sharded && H->nranks > 1 && H->comm) {
     double *d = H->red;  // reuse: [-min, max, bad]
     double v[3] = {-out[0], out[1], out[2]};
     CUDA_TRY(cudaMemcpyAsync(d, v, sizeof(v), cudaMemcpyHostToDevice, st));
@@ -666,6 +751,13 @@ nlse2shoc_status nlse2shoc_create_sharded(nlse2shoc_t *out, int dims, const int6
   return create_impl(out, dims, N, h, a, s, V, bc, dtype, rank, nranks, id128);
 }
 
+nlse2shoc_status nlse2shoc_create_loopback(nlse2shoc_t *out, int dims, const int64_t N[3], const double h[3],
+                                           double a, double s, const nlse2shoc_potential *V, nlse2shoc_bc bc,
+                                           nlse2shoc_dtype dtype, int nslabs) {
+  if (nslabs < 1) return fail(NLSE2SHOC_EINVAL, "nslabs must be >= 1");
+  return create_impl(out, dims, N, h, a, s, V, bc, dtype, 0, 1, nullptr, -nslabs);
+}
+
 nlse2shoc_status nlse2shoc_local_extent(nlse2shoc_t H, int64_t *z0, int64_t *nz) {
   if (!H || !z0 || !nz) return fail(NLSE2SHOC_EINVAL, "NULL argument");
   *z0 = H->dims >= 2 ? H->z0 : 0;
@@ -673,12 +765,18 @@ nlse2shoc_status nlse2shoc_local_extent(nlse2shoc_t H, int64_t *z0, int64_t *nz)
   return NLSE2SHOC_OK;
 }
 
-size_t nlse2shoc_workspace_bytes(nlse2shoc_t H) { return H ? H->bytes : 0; }
+size_t nlse2shoc_workspace_bytes(nlse2shoc_t H) {
+  if (!H) return 0;
+  size_t b = H->bytes;
+  for (nlse2shoc_t S : H->slabs) b += S->bytes;
+  return b;
+}
 
 nlse2shoc_status nlse2shoc_set_variant(nlse2shoc_t H, int variant) {
   if (!H) return fail(NLSE2SHOC_EINVAL, "NULL handle");
   if (variant != 0 && variant != 1) return fail(NLSE2SHOC_EINVAL, "variant must be 0 (fused) or 1 (two-kernel)");
-  if (variant == 1) TRY(ensure_D(H));
+  for (nlse2shoc_t S : H->slabs) TRY(nlse2shoc_set_variant(S, variant));
+  if (variant == 1 && H->slabs.empty()) TRY(ensure_D(H));
   H->variant = variant;
   return NLSE2SHOC_OK;
 }
@@ -689,26 +787,20 @@ nlse2shoc_status nlse2shoc_laplacian(nlse2shoc_t H, const void *psi, void *L, vo
   TRY(check_ptr(L, "L"));
   if (psi == L) return fail(NLSE2SHOC_EINVAL, "psi and L must be distinct");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  H->launches = 0;
-  Field w;
-  TRY(psi_in(H, const_cast<void *>(psi), w, st));
-  void *dst = H->pitch == H->nx ? L : H->TA.ptr;
-  const bool f64 = H->dtype == NLSE2SHOC_C64;
-  if (H->variant == 0) {
-    switch (H->dims) {
-      case 1: TRY(f64 ? (lap_fused<1, float>(H, w, dst, st)) : (lap_fused<1, double>(H, w, dst, st))); break;
-      case 2: TRY(f64 ? (lap_fused<2, float>(H, w, dst, st)) : (lap_fused<2, double>(H, w, dst, st))); break;
-      default: TRY(f64 ? (lap_fused<3, float>(H, w, dst, st)) : (lap_fused<3, double>(H, w, dst, st))); break;
-    }
-  } else {
-    switch (H->dims) {
-      case 1: TRY(f64 ? (lap_two<1, float>(H, w, dst, st)) : (lap_two<1, double>(H, w, dst, st))); break;
-      case 2: TRY(f64 ? (lap_two<2, float>(H, w, dst, st)) : (lap_two<2, double>(H, w, dst, st))); break;
-      default: TRY(f64 ? (lap_two<3, float>(H, w, dst, st)) : (lap_two<3, double>(H, w, dst, st))); break;
-    }
+  reset_launches(H);
+  View v;
+  void *work = nullptr;
+  TRY(make_view(H, const_cast<void *>(psi), v, &work, st));
+  // output: the caller's L directly, or the pitched staging buffer
+  void *dst = H->pitch == H->nx ? L : H->Lw;
+  TRY(exchange(v, 5, st));
+  for (size_t i = 0; i < v.hs.size(); ++i) {
+    nlse2shoc_t S = v.hs[i];
+    // loopback slabs write their part of the full L; a real shard owns the whole local L
+    void *Li = H->slabs.empty() ? dst : reinterpret_cast<char *>(dst) + size_t(S->z0) * S->plane * S->S;
+    TRY(stage(S, v.psis[i], 5, 0.0, Li, st));
   }
-  if (dst != L) TRY(psi_out(H, L, dst, st));
-  return NLSE2SHOC_OK;
+  return unstage(H, L, dst, st);
 }
 
 nlse2shoc_status nlse2shoc_rk4(nlse2shoc_t H, void *psi, double dt, int64_t nsteps, void *stream) {
@@ -717,25 +809,13 @@ nlse2shoc_status nlse2shoc_rk4(nlse2shoc_t H, void *psi, double dt, int64_t nste
   if (!finite_pos(dt)) return fail(NLSE2SHOC_EINVAL, "dt must be finite and > 0");
   if (nsteps < 0) return fail(NLSE2SHOC_EINVAL, "nsteps must be >= 0");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  H->launches = 0;
+  reset_launches(H);
   if (nsteps == 0) return NLSE2SHOC_OK;
-  Field w;
-  TRY(psi_in(H, psi, w, st));
-  const bool f64 = H->dtype == NLSE2SHOC_C64;
-  if (H->variant == 0) {
-    switch (H->dims) {
-      case 1: TRY(f64 ? (rk4_fused<1, float>(H, w, dt, nsteps, st)) : (rk4_fused<1, double>(H, w, dt, nsteps, st))); break;
-      case 2: TRY(f64 ? (rk4_fused<2, float>(H, w, dt, nsteps, st)) : (rk4_fused<2, double>(H, w, dt, nsteps, st))); break;
-      default: TRY(f64 ? (rk4_fused<3, float>(H, w, dt, nsteps, st)) : (rk4_fused<3, double>(H, w, dt, nsteps, st))); break;
-    }
-  } else {
-    switch (H->dims) {
-      case 1: TRY(f64 ? (rk4_two<1, float>(H, w, dt, nsteps, st)) : (rk4_two<1, double>(H, w, dt, nsteps, st))); break;
-      case 2: TRY(f64 ? (rk4_two<2, float>(H, w, dt, nsteps, st)) : (rk4_two<2, double>(H, w, dt, nsteps, st))); break;
-      default: TRY(f64 ? (rk4_two<3, float>(H, w, dt, nsteps, st)) : (rk4_two<3, double>(H, w, dt, nsteps, st))); break;
-    }
-  }
-  return psi_out(H, psi, w.ptr, st);
+  View v;
+  void *work = nullptr;
+  TRY(make_view(H, psi, v, &work, st));
+  TRY(run_rk4(v, dt, nsteps, st));
+  return unstage(H, psi, work, st);
 }
 
 nlse2shoc_status nlse2shoc_stability_bound(nlse2shoc_t H, const void *psi, double *kmax, void *stream) {
@@ -769,7 +849,12 @@ nlse2shoc_status nlse2shoc_check_finite(nlse2shoc_t H, const void *psi, void *st
   return NLSE2SHOC_OK;
 }
 
-int64_t nlse2shoc_last_launch_count(nlse2shoc_t H) { return H ? H->launches : -1; }
+int64_t nlse2shoc_last_launch_count(nlse2shoc_t H) {
+  if (!H) return -1;
+  int64_t n = H->launches;
+  for (nlse2shoc_t S : H->slabs) n += S->launches;
+  return n;
+}
 
 const char *nlse2shoc_strerror(nlse2shoc_status st) {
   const int i = -int(st);
@@ -790,6 +875,8 @@ const char *nlse2shoc_version(void) {
 void nlse2shoc_destroy(nlse2shoc_t H) {
   if (!H) return;
   cudaDeviceSynchronize();
+  for (nlse2shoc_t S : H->slabs) nlse2shoc_destroy(S);
+  if (H->Lw) cudaFree(H->Lw);
   for (Field *f : {&H->TA, &H->TB, &H->acc, &H->psiw, &H->D}) {
     if (f->ptr) cudaFree(f->ptr);
     if (f->halo_lo) cudaFree(f->halo_lo);

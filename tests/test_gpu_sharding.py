@@ -1,0 +1,74 @@
+"""Sharded path on one GPU (SURVEY §4 T3'): the loopback handle splits the slowest axis into
+virtual slabs exactly like the NCCL shards (nlse2shoc_split), exchanges 2-plane halos by
+device copies and runs the same kernels.  The step has no reductions and halos are exact
+copies, so results must be BITWISE equal to the single-slab handle."""
+import numpy as np
+import pytest
+
+from icgen import configs
+
+import harness as H
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def _run(work, dtype, shard, variant, nsteps, dt, psi0, lap=False):
+    import paper_1109_1027_b200 as nl
+
+    Varr = H.V_array_device(work, dtype) if work["V"]["kind"] == "array" else None
+    S = nl.solver_from_work(work, dtype, V_array=Varr, shard=shard)
+    if variant:
+        S.set_variant(variant)
+    g = torch.from_numpy(psi0).cuda()
+    if lap:
+        out = S.laplacian(g).cpu().numpy()
+    else:
+        S.rk4(g, dt, nsteps)
+        out = g.cpu().numpy()
+    k = S.stability_bound(torch.from_numpy(psi0).cuda())
+    S.close()
+    return out, k
+
+
+CASES = [
+    (3, (37, 19, 23), "dirichlet", "c64", "harmonic"),
+    (3, (40, 33, 31), "lapzero", "c128", "none"),
+    (3, (21, 18, 29), "dirichlet", "c128", "array"),
+    (2, (70, 61), "dirichlet", "c128", "harmonic"),
+    (2, (531, 17), "lapzero", "c64", "none"),
+]
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("nslabs", [2, 3, 7])
+@pytest.mark.parametrize("dims,n,bc,dtype,V", CASES)
+def test_loopback_bitwise_equal(dims, n, bc, dtype, V, nslabs, variant):
+    w = configs.SMALL(dims, n, bc, dtype=dtype, V=V, noise=0.05)
+    psi0 = H.psi0_host(w, dtype)
+    ref, k1 = _run(w, dtype, None, variant, 6, 1e-4, psi0)
+    got, kP = _run(w, dtype, {"loopback": nslabs}, variant, 6, 1e-4, psi0)
+    assert np.array_equal(got.view(np.uint8), ref.view(np.uint8))
+    assert kP == k1
+    lref, _ = _run(w, dtype, None, variant, 0, 1.0, psi0, lap=True)
+    lgot, _ = _run(w, dtype, {"loopback": nslabs}, variant, 0, 1.0, psi0, lap=True)
+    assert np.array_equal(lgot.view(np.uint8), lref.view(np.uint8))
+
+
+def test_loopback_C4_full_size_matches_single_gpu():
+    """C4's 768^3 grid split like an 8-GPU run (96 planes per slab)."""
+    w = configs.C4()
+    S1 = H.gpu_solver(w, "c64")
+    torch.manual_seed(0)
+    psi = torch.randn(768, 768, 768, dtype=torch.complex64, device="cuda") * 0.01 + 1.0
+    dt = 0.8 * S1.stability_bound(psi)
+    a = psi.clone()
+    S1.rk4(a, dt, 2)
+    S1.close()
+    import paper_1109_1027_b200 as nl
+
+    S8 = nl.solver_from_work(w, "c64", shard={"loopback": 8})
+    b = psi.clone()
+    S8.rk4(b, dt, 2)
+    assert torch.equal(torch.view_as_real(a), torch.view_as_real(b))
+    S8.close()
