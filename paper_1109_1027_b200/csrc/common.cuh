@@ -5,6 +5,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 namespace nlse {
 
@@ -58,16 +59,42 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
   return ok != 0;
 }
 
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t *bar, uint32_t parity, uint32_t ns);
+#ifdef NLSE_DEBUG_HANG
+#define NLSE_HANG_CHECK(tag)                                                                              \
+  if (++spins_ == (1u << 22))                                                                            \
+    printf("hang? %s block %d thread %d bar %p parity %u\n", tag, blockIdx.x, threadIdx.x, (void *)bar, parity);
+#else
+#define NLSE_HANG_CHECK(tag)
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) {
+  if (mbar_try_wait(bar, parity)) return;  // fast path: phase already complete
+  uint32_t spins_ = 0;
+  (void)spins_;
+  while (!mbar_try_wait_sleep(bar, parity, 20000)) {
+    NLSE_HANG_CHECK("consumer")
   }
 }
 
-// Producer-side wait: back off between polls so the waiting warp does not steal issue
-// slots from the consumer warps of its scheduler.
+// Suspending wait: try_wait with a suspend-time hint parks the warp in hardware until the
+// phase completes (or the hint expires) instead of spinning, so a waiting warp does not
+// steal issue slots from the working warps of its scheduler.
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t *bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait_backoff(uint64_t *bar, uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) {
-    __nanosleep(256);
+  uint32_t spins_ = 0;
+  (void)spins_;
+  while (!mbar_try_wait_sleep(bar, parity, 20000)) {
+    NLSE_HANG_CHECK("producer")
   }
 }
 
@@ -122,6 +149,15 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
 // streaming (evict-first) 128-bit global stores: outputs are re-read only by the next stage
 __device__ __forceinline__ void st_stream(float4 *p, float4 v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(double2 *p, double2 v) { __stcs(p, v); }
+
+__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu(uint32_t *p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

@@ -96,6 +96,10 @@ struct nlse2shoc_s {
   size_t bytes = 0;
   int num_sms = 148;
   int64_t launches = 0;
+  uint32_t *prog = nullptr;  // per-tile progress words of the stage kernel (neighbour coupling)
+  int prog_cap = 0;
+  uint32_t epoch = 0;
+  uint32_t *rbar = nullptr;  // round-barrier counter of the stage kernel
   // loopback (single-GPU emulation of z-slab sharding, SURVEY §4 T3'): virtual slabs that
   // exchange halos by device copies instead of NCCL; empty for ordinary handles
   std::vector<nlse2shoc_s *> slabs;
@@ -236,9 +240,32 @@ static nlse2shoc_status launch_stream(nlse2shoc_t H, Field &in, const CUtensorMa
     const double c = rounds * len;
     if (c < bestc - 1e-9) { bestc = c; best = nc; }
   }
+  static const int force_chunks = getenv("NLSE_NCHUNK") ? atoi(getenv("NLSE_NCHUNK")) : 0;
+  if (force_chunks > 0) best = std::min<int>(force_chunks, int(H->nz));
   P.nchunk = best;
   P.ntiles = ncol * best;
   const int G = std::min(G0, P.ntiles);
+  // neighbour coupling (NLSE_LEAD=0 disables): per-tile progress words, epoch-tagged
+  static const int lead = getenv("NLSE_LEAD") ? atoi(getenv("NLSE_LEAD")) : 0;
+  static const int rbar = getenv("NLSE_RBAR") ? atoi(getenv("NLSE_RBAR")) : 0;
+  if (rbar && P.ntiles > G) {
+    if (!H->rbar) CUDA_TRY(cudaMalloc(&H->rbar, 256));
+    CUDA_TRY(cudaMemsetAsync(H->rbar, 0, sizeof(uint32_t), st));
+    P.rbar = H->rbar;
+  }
+  if (lead > 0) {
+    if (H->prog_cap < P.ntiles) {
+      if (H->prog) cudaFree(H->prog);
+  if (H->rbar) cudaFree(H->rbar);
+      CUDA_TRY(cudaMalloc(&H->prog, sizeof(uint32_t) * P.ntiles));
+      CUDA_TRY(cudaMemsetAsync(H->prog, 0, sizeof(uint32_t) * P.ntiles, st));
+      H->prog_cap = P.ntiles;
+    }
+    H->epoch = (H->epoch + 1) & 0xffff;
+    P.prog = H->prog;
+    P.epoch = H->epoch;
+    P.lead = lead;
+  }
   const CUtensorMap *lo = P.has_lo_halo ? &in.tm_lo : &in.tm;
   const CUtensorMap *hi = P.has_hi_halo ? &in.tm_hi : &in.tm;
   stage_stream_kernel<DIMS, R, MODE><<<G, LY::NTHREADS, smem, st>>>(in.tm, *lo, *hi, tm_psi ? *tm_psi : in.tm,
@@ -883,6 +910,8 @@ void nlse2shoc_destroy(nlse2shoc_t H) {
     if (f->halo_hi) cudaFree(f->halo_hi);
   }
   if (H->vtab) cudaFree(H->vtab);
+  if (H->prog) cudaFree(H->prog);
+  if (H->rbar) cudaFree(H->rbar);
   if (H->red) cudaFree(H->red);
 #ifdef NLSE_WITH_NCCL
   if (H->comm) ncclCommDestroy(H->comm);

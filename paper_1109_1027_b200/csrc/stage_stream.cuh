@@ -22,6 +22,10 @@
 #pragma once
 #include <type_traits>
 
+#ifndef NLSE_LEAN_DIMS
+#define NLSE_LEAN_DIMS 3
+#endif
+
 #include "common.cuh"
 
 namespace nlse {
@@ -92,6 +96,10 @@ template <typename R> struct StageParams {
   int vkind;             // 0 none, 1 harmonic tables, 2 array
   const R *vx, *vy, *vz; // harmonic tables (vz indexed by GLOBAL streamed index)
   const R *varr;         // array potential (local slab, row pitch nx)
+  uint32_t *prog;        // per-tile producer progress (epoch << 16 | planes issued), or null
+  uint32_t epoch;        // launch tag of this stage's progress words
+  int lead;              // max planes a tile's producer may run ahead of its neighbours
+  uint32_t *rbar;        // round barrier counter (producers start each round together), or null
   cplx<R> *out_T;        // T_s (stages 1-3), psi^{n+1} (stage 4), L (laplacian mode)
   cplx<R> *out_acc;      // accumulator (stages 1-3)
 };
@@ -239,9 +247,42 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
         const int chunk = t / ncol, col = t % ncol;
         const int x0 = (col % P.ncx) * TX, y0 = (col / P.ncx) * TY;
         const int kb = chunk * chunk_len, ke = min(P.nz, kb + chunk_len);
+        // Round barrier: every producer starts round r only after all producers finished
+        // issuing round r-1, so the tiles of a round stream the same planes at the same time
+        // and a tile's halo rows/columns are L2 hits when its neighbours load them.
+        if (P.rbar && t >= G) {
+          const uint32_t need = uint32_t(t / G) * uint32_t(G);
+          while (ld_relaxed_gpu(P.rbar) < need) __nanosleep(64);
+        }
+        // Neighbour coupling: tiles that share halo data with this one and run in the same
+        // round keep their producers within `lead` planes of each other, so one tile's halo
+        // rows/columns are still in L2 when its neighbour streams the same plane.
+        int nb[4], nnb = 0;
+        if (P.prog) {
+          const int round = t / G, cx = col % P.ncx, cyy = col / P.ncx;
+          const int cand[4] = {cx > 0 ? t - 1 : -1, cx + 1 < P.ncx ? t + 1 : -1, cyy > 0 ? t - P.ncx : -1,
+                               cyy + 1 < P.ncy ? t + P.ncx : -1};
+          for (int i = 0; i < 4; ++i)
+            if (cand[i] >= 0 && cand[i] < P.ntiles && cand[i] / G == round) nb[nnb++] = cand[i];
+        }
+        int issued = 0, seen = 0;  // planes issued for this tile; min neighbour progress seen
+        auto gate = [&](int j) {
+          if (nnb == 0 || j - P.lead <= seen) return;
+          for (int spin = 0; spin < 4000; ++spin) {
+            int m = 1 << 30;
+            for (int i = 0; i < nnb; ++i) {
+              const uint32_t v = ld_relaxed_gpu(P.prog + nb[i]);
+              m = min(m, (v >> 16) == P.epoch ? int(v & 0xffff) : 0);
+            }
+            seen = m;
+            if (j - P.lead <= seen) return;
+            __nanosleep(100);
+          }
+        };
         auto produceT = [&](int p) {
           const uint32_t slot = tcnt % RT, par = (tcnt / RT) & 1;
           mbar_wait_backoff(&emptyT[slot], par ^ 1);
+          gate(issued);
           const CUtensorMap *m = nullptr;
           int pz = p;
           if (p >= 0 && p < P.nz) m = &tm_T;
@@ -261,6 +302,8 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
             mbar_arrive(&fullT[slot]);
           }
           ++tcnt;
+          ++issued;
+          if (P.prog) st_relaxed_gpu(P.prog + t, (P.epoch << 16) | uint32_t(issued));
         };
         auto produceP = [&](int k) {
           const uint32_t slot = pcnt % RPM, par = (pcnt / RPM) & 1;
@@ -287,6 +330,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
           produceT(k + 2);
           if (NPA) produceP(k);
         }
+        if (P.rbar) atomicAdd(P.rbar, 1u);
       }
     }
     return;
@@ -353,7 +397,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
     cplx<R> *outT = P.out_T + int64_t(kb) * P.plane + int64_t(y0 + ly0) * P.pitch + (x0 + lx0);
     cplx<R> *outA = (MODE != M_LAP && MODE != M_S4) ? P.out_acc + (outT - P.out_T) : nullptr;
 
-    for (int k = kb; k < ke; ++k) {
+    auto general_step = [&](int k) {
       const int gz = z0 + k;  // global streamed index
       const R vzk = (P.vkind == 1 && P.vz) ? P.vz[gz] : R(0);
       mbar_wait(&fullT[sk2], ph2);
@@ -535,6 +579,107 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
       sk = inc(sk, RT);
       sk2 = inc(sk2, RT);
       ph2 ^= sk2 == 0;
+    };
+
+    // ---- lean plane step: tile interior in x/y, plane at least 2 away from the streamed
+    // faces (no boundary point, no ghost): straight-line loads, arithmetic and stores.
+    const CT *ringT = ring + toff;
+    const int64_t pitch = P.pitch, plane = P.plane;
+    const R vzero = R(0);
+    auto lean_step = [&](int k) {
+      const int gz = z0 + k;
+      const R vzk = (P.vkind == 1 && P.vz) ? P.vz[gz] : vzero;
+      mbar_wait(&fullT[sk2], ph2);
+      const CT *pa = nullptr;
+      if (NPA) {
+        mbar_wait(&fullP[sp], php);
+        pa = pring + size_t(sp) * NPA * LY::PTILE + ly0 * TX + lx0;
+      }
+      const CT *s0 = ringT + size_t(sk) * LY::SLOT, *sp2 = ringT + size_t(sk2) * LY::SLOT;
+#pragma unroll
+      for (int r = 0; r < RPW; ++r) {
+        CT run[PPX + 4];
+        lds_run<R, PPX + 4>(s0 + r * W, run);
+        CT zp2[PPX];
+        lds_run<R, PPX>(sp2 + r * W + 2, zp2);
+        CT ym2[PPX], ym1[PPX], yp1[PPX], yp2[PPX];
+        if (DIMS == 3) {
+          lds_run<R, PPX>(s0 + (r - 2) * W + 2, ym2);
+          lds_run<R, PPX>(s0 + (r - 1) * W + 2, ym1);
+          lds_run<R, PPX>(s0 + (r + 1) * W + 2, yp1);
+          lds_run<R, PPX>(s0 + (r + 2) * W + 2, yp2);
+        }
+        CT psv[PPX], acv[PPX];
+        if (LY::template needs_psi<MODE>()) lds_run<R, PPX>(pa + r * TX, psv);
+        if (LY::template needs_acc<MODE>()) lds_run<R, PPX>(pa + ACC_OFF + r * TX, acv);
+        CT oT[PPX], oA[PPX];
+#pragma unroll
+        for (int q = 0; q < PPX; ++q) {
+          const CT c = run[q + 2];
+          CT L = cx * (R(16) * (run[q + 1] + run[q + 3]) - (run[q] + run[q + 4]));
+          L = L + cz * (R(16) * (qm1[r][q] + qp1[r][q]) - (qm2[r][q] + zp2[q]));
+          if (DIMS == 3) L = L + cy * (R(16) * (ym1[q] + yp1[q]) - (ym2[q] + yp2[q]));
+          L = axpy(L, -c30, c);
+          R V;
+          if (P.vkind == 2) V = potential(P, x0 + lx0 + q, y0 + ly0 + r, k);
+          else V = (vxr[q] + vyr[r]) + vzk;
+          const R N = fma(ps_, norm2(c), -V);
+          const CT F = mk<R>(-fma(pa_, L.im, N * c.im), fma(pa_, L.re, N * c.re));  // i (a L + N c)
+          if (MODE == M_LAP) {
+            oT[q] = L;
+          } else if (MODE == M_S1) {
+            oA[q] = axpy(c, ca, F);
+            oT[q] = axpy(c, cb, F);
+          } else if (MODE == M_S2 || MODE == M_S3) {
+            oA[q] = axpy(acv[q], ca, F);
+            oT[q] = axpy(psv[q], cb, F);
+          } else {
+            oT[q] = axpy(acv[q], cb, F);
+          }
+        }
+        using VV = V16<R>;
+#pragma unroll
+        for (int v = 0; v < PPX / VV::CPV; ++v) {
+          st_stream(reinterpret_cast<typename VV::T *>(outT + r * pitch) + v, VV::join(oT + v * VV::CPV));
+          if (MODE != M_LAP && MODE != M_S4)
+            st_stream(reinterpret_cast<typename VV::T *>(outA + r * pitch) + v, VV::join(oA + v * VV::CPV));
+        }
+#pragma unroll
+        for (int q = 0; q < PPX; ++q) {
+          qm2[r][q] = qm1[r][q];
+          qm1[r][q] = run[q + 2];
+          qp1[r][q] = zp2[q];
+        }
+      }
+      outT += plane;
+      if (MODE != M_LAP && MODE != M_S4) outA += plane;
+      __syncwarp();
+      if (NPA) {
+        if (lane == 0) mbar_arrive(&emptyP[sp]);
+        sp = inc(sp, RPM);
+        php ^= sp == 0;
+      }
+      if (lane == 0) mbar_arrive(&emptyT[skm1]);
+      skm1 = inc(skm1, RT);
+      sk = inc(sk, RT);
+      sk2 = inc(sk2, RT);
+      ph2 ^= sk2 == 0;
+    };
+
+#ifndef NLSE_NO_LEAN
+#define NLSE_LEAN_OK true
+#else
+#define NLSE_LEAN_OK false
+#endif
+    if (inner_xy && NLSE_LEAN_OK && (NLSE_LEAN_DIMS & DIMS)) {
+      // lean planes: gz in [2, NZ-3], clamped to this tile's chunk [kb, ke)
+      const int l0 = min(ke, max(kb, 2 - z0)), l1 = max(l0, min(ke, NZ - 2 - z0));
+      int k = kb;
+      for (; k < l0; ++k) general_step(k);
+      for (; k < l1; ++k) lean_step(k);
+      for (; k < ke; ++k) general_step(k);
+    } else {
+      for (int k = kb; k < ke; ++k) general_step(k);
     }
     pcnt += uint32_t(ke - kb) * (NPA ? 1 : 0);
     __syncwarp();

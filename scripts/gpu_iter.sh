@@ -1,6 +1,6 @@
 # quick iteration: parity tests, then bench, then a launch-list ncu pass
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke_rc=$?; tail -1 gpurun_out/smoke.log
-timeout 1500 python -m pytest tests/test_gpu_parity.py -q -m gpu --timeout 600 -x > gpurun_out/gpu_all.log 2>&1; echo tests_rc=$?; tail -4 gpurun_out/gpu_all.log
+timeout 1500 python -m pytest tests/test_gpu_parity.py -q -m gpu --timeout 120 -x > gpurun_out/gpu_all.log 2>&1; echo tests_rc=$?; tail -4 gpurun_out/gpu_all.log
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench_rc=$?
 cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err
 if [ "$NCU" = "1" ]; then
