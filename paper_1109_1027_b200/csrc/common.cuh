@@ -20,6 +20,26 @@ template <typename R> __device__ __forceinline__ cplx<R> axpy(cplx<R> a, R s, cp
   return {fma(s, b.re, a.re), fma(s, b.im, a.im)};
 }
 template <typename R> __device__ __forceinline__ R norm2(cplx<R> a) { return fma(a.re, a.re, a.im * a.im); }
+// a + s * (i t)  (the RK4 stage combine with F = i t)
+template <typename R> __device__ __forceinline__ cplx<R> iaxpy(cplx<R> a, R s, cplx<R> t) {
+  return {fma(-s, t.im, a.re), fma(s, t.re, a.im)};
+}
+
+// complex64: packed FP32x2 arithmetic (sm_100 FADD2 / FMUL2 / FFMA2 on the (re, im) pair),
+// one instruction per complex operation instead of two.
+__device__ __forceinline__ float2 f2(cplx<float> a) { return make_float2(a.re, a.im); }
+__device__ __forceinline__ cplx<float> c2(float2 a) { return {a.x, a.y}; }
+__device__ __forceinline__ cplx<float> operator+(cplx<float> a, cplx<float> b) { return c2(__fadd2_rn(f2(a), f2(b))); }
+__device__ __forceinline__ cplx<float> operator-(cplx<float> a, cplx<float> b) {
+  return c2(__ffma2_rn(f2(b), make_float2(-1.f, -1.f), f2(a)));
+}
+__device__ __forceinline__ cplx<float> operator*(float s, cplx<float> a) { return c2(__fmul2_rn(make_float2(s, s), f2(a))); }
+__device__ __forceinline__ cplx<float> axpy(cplx<float> a, float s, cplx<float> b) {
+  return c2(__ffma2_rn(f2(b), make_float2(s, s), f2(a)));
+}
+__device__ __forceinline__ cplx<float> iaxpy(cplx<float> a, float s, cplx<float> t) {
+  return c2(__ffma2_rn(make_float2(t.im, t.re), make_float2(-s, s), f2(a)));
+}
 
 // ---------------------------------------------------------------------------------- PTX
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -147,8 +167,19 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
 }
 
 // streaming (evict-first) 128-bit global stores: outputs are re-read only by the next stage
+#ifndef NLSE_STORE_KIND
+#define NLSE_STORE_KIND 0
+#endif
+#if NLSE_STORE_KIND == 1
 __device__ __forceinline__ void st_stream(float4 *p, float4 v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(double2 *p, double2 v) { __stcs(p, v); }
+#elif NLSE_STORE_KIND == 2
+__device__ __forceinline__ void st_stream(float4 *p, float4 v) { __stwt(p, v); }
+__device__ __forceinline__ void st_stream(double2 *p, double2 v) { __stwt(p, v); }
+#else
+__device__ __forceinline__ void st_stream(float4 *p, float4 v) { *p = v; }
+__device__ __forceinline__ void st_stream(double2 *p, double2 v) { *p = v; }
+#endif
 
 __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t *p) {
   uint32_t v;

@@ -349,6 +349,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
   const int ly0 = rg * RPW;                        // first local row of this thread
   const CT zero = mk<R>(R(0), R(0));
   const R cx = P.cx, cy = P.cy, cz = P.cz, c30 = P.c30, pa_ = P.a, ps_ = P.s, ca = P.ca, cb = P.cb;
+  const R c16x = R(16) * cx, c16y = R(16) * cy, c16z = R(16) * cz;
   const int nx = P.nx, ny = P.ny, nz = P.nz, NZ = P.NZ, z0 = P.z0;
   uint32_t tcnt = 0, pcnt = 0;
   auto inc = [](int v, int m) { return v + 1 == m ? 0 : v + 1; };
@@ -397,9 +398,18 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
     cplx<R> *outT = P.out_T + int64_t(kb) * P.plane + int64_t(y0 + ly0) * P.pitch + (x0 + lx0);
     cplx<R> *outA = (MODE != M_LAP && MODE != M_S4) ? P.out_acc + (outT - P.out_T) : nullptr;
 
+    // streamed-axis potential table, software-pipelined one plane ahead (its global load
+    // would otherwise sit on the critical path of every plane)
+    const bool has_vz = P.vkind == 1 && P.vz;
+    R vz_pre = has_vz ? P.vz[z0 + kb] : R(0);
+    auto vz_next = [&](int k) -> R {
+      const R v = vz_pre;
+      if (has_vz && k + 1 < ke) vz_pre = P.vz[z0 + k + 1];
+      return v;
+    };
     auto general_step = [&](int k) {
       const int gz = z0 + k;  // global streamed index
-      const R vzk = (P.vkind == 1 && P.vz) ? P.vz[gz] : R(0);
+      const R vzk = vz_next(k);
       mbar_wait(&fullT[sk2], ph2);
       const CT *pa = nullptr;
       if (NPA) {
@@ -502,39 +512,44 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
         for (int q = 0; q < PPX; ++q) {
           const int gx = x0 + lx0 + q;
           const CT c = run[q + 2];
-          // 5-point wide form per axis, (16 (g-1 + g+1) - (g-2 + g+2) - 30 g0) / (12 h^2)
-          CT L = cx * (R(16) * (run[q + 1] + run[q + 3]) - (run[q] + run[q + 4]));
-          L = L + cz * (R(16) * (qm1[r][q] + qp1[r][q]) - (qm2[r][q] + zp2[q]));
-          if (DIMS == 3) L = L + cy * (R(16) * (ym1[q] + yp1[q]) - (ym2[q] + yp2[q]));
-          L = axpy(L, -c30, c);
+          // 5-point wide form per axis: sum_d (16 (g-1 + g+1) - (g-2 + g+2) - 30 g0) / (12 h_d^2)
+          CT L = (-c30) * c;
+          L = axpy(L, c16x, run[q + 1] + run[q + 3]);
+          L = axpy(L, -cx, run[q] + run[q + 4]);
+          L = axpy(L, c16z, qm1[r][q] + qp1[r][q]);
+          L = axpy(L, -cz, qm2[r][q] + zp2[q]);
+          if (DIMS == 3) {
+            L = axpy(L, c16y, ym1[q] + yp1[q]);
+            L = axpy(L, -cy, ym2[q] + yp2[q]);
+          }
           R V;
           if (P.vkind == 2) V = (gx < nx && gy < ny) ? potential(P, gx, gy, k) : R(0);
           else V = (vxr[q] + vyr[r]) + vzk;
           const R N = fma(ps_, norm2(c), -V);
-          CT F;
+          CT tF;  // F = i tF
           if (fast) {
             valid[q] = true;
-            F = mk<R>(-fma(pa_, L.im, N * c.im), fma(pa_, L.re, N * c.re));  // i (a L + N c)
+            tF = axpy(N * c, pa_, L);  // a L + N c
           } else {
             valid[q] = gx < nx && gy < ny;
             const bool bnd = gx == 0 || gx == nx - 1 || (DIMS == 3 && (gy == 0 || gy == ny - 1)) || !zint;
             if (!bnd) {
-              F = mk<R>(-fma(pa_, L.im, N * c.im), fma(pa_, L.re, N * c.re));
+              tF = axpy(N * c, pa_, L);
             } else {
               L = lambda_b(P, c, V);
-              F = P.bc == 0 ? zero : mk<R>(-(N * c.im), N * c.re);
+              tF = P.bc == 0 ? zero : N * c;
             }
           }
           if (MODE == M_LAP) {
             oT[q] = L;
           } else if (MODE == M_S1) {
-            oA[q] = axpy(c, ca, F);
-            oT[q] = axpy(c, cb, F);
+            oA[q] = iaxpy(c, ca, tF);
+            oT[q] = iaxpy(c, cb, tF);
           } else if (MODE == M_S2 || MODE == M_S3) {
-            oA[q] = axpy(acv[q], ca, F);
-            oT[q] = axpy(psv[q], cb, F);
+            oA[q] = iaxpy(acv[q], ca, tF);
+            oT[q] = iaxpy(psv[q], cb, tF);
           } else {  // M_S4
-            oT[q] = axpy(acv[q], cb, F);
+            oT[q] = iaxpy(acv[q], cb, tF);
           }
         }
         // ---- stores (128-bit when all PPX points are inside the grid)
@@ -585,10 +600,9 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
     // faces (no boundary point, no ghost): straight-line loads, arithmetic and stores.
     const CT *ringT = ring + toff;
     const int64_t pitch = P.pitch, plane = P.plane;
-    const R vzero = R(0);
     auto lean_step = [&](int k) {
       const int gz = z0 + k;
-      const R vzk = (P.vkind == 1 && P.vz) ? P.vz[gz] : vzero;
+      const R vzk = vz_next(k);
       mbar_wait(&fullT[sk2], ph2);
       const CT *pa = nullptr;
       if (NPA) {
@@ -616,25 +630,30 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
 #pragma unroll
         for (int q = 0; q < PPX; ++q) {
           const CT c = run[q + 2];
-          CT L = cx * (R(16) * (run[q + 1] + run[q + 3]) - (run[q] + run[q + 4]));
-          L = L + cz * (R(16) * (qm1[r][q] + qp1[r][q]) - (qm2[r][q] + zp2[q]));
-          if (DIMS == 3) L = L + cy * (R(16) * (ym1[q] + yp1[q]) - (ym2[q] + yp2[q]));
-          L = axpy(L, -c30, c);
+          CT L = (-c30) * c;
+          L = axpy(L, c16x, run[q + 1] + run[q + 3]);
+          L = axpy(L, -cx, run[q] + run[q + 4]);
+          L = axpy(L, c16z, qm1[r][q] + qp1[r][q]);
+          L = axpy(L, -cz, qm2[r][q] + zp2[q]);
+          if (DIMS == 3) {
+            L = axpy(L, c16y, ym1[q] + yp1[q]);
+            L = axpy(L, -cy, ym2[q] + yp2[q]);
+          }
           R V;
           if (P.vkind == 2) V = potential(P, x0 + lx0 + q, y0 + ly0 + r, k);
           else V = (vxr[q] + vyr[r]) + vzk;
           const R N = fma(ps_, norm2(c), -V);
-          const CT F = mk<R>(-fma(pa_, L.im, N * c.im), fma(pa_, L.re, N * c.re));  // i (a L + N c)
+          const CT tF = axpy(N * c, pa_, L);  // F = i (a L + N c)
           if (MODE == M_LAP) {
             oT[q] = L;
           } else if (MODE == M_S1) {
-            oA[q] = axpy(c, ca, F);
-            oT[q] = axpy(c, cb, F);
+            oA[q] = iaxpy(c, ca, tF);
+            oT[q] = iaxpy(c, cb, tF);
           } else if (MODE == M_S2 || MODE == M_S3) {
-            oA[q] = axpy(acv[q], ca, F);
-            oT[q] = axpy(psv[q], cb, F);
+            oA[q] = iaxpy(acv[q], ca, tF);
+            oT[q] = iaxpy(psv[q], cb, tF);
           } else {
-            oT[q] = axpy(acv[q], cb, F);
+            oT[q] = iaxpy(acv[q], cb, tF);
           }
         }
         using VV = V16<R>;
