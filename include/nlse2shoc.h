@@ -119,10 +119,15 @@ nlse2shoc_status nlse2shoc_split(int64_t n_slow, int nranks, int rank, int64_t *
 size_t nlse2shoc_workspace_bytes(nlse2shoc_t);
 
 /* 0 = FUSED (default): one kernel per RK4 stage computes the whole 2SHOC Laplacian (both
- *     steps, D never stored), the RHS and the RK4 stage combine.
+ *     steps, D never stored), the RHS and the RK4 stage combine.  2D/3D use the
+ *     reconstructed-accumulator form: stage 1 stores only T_A = Psi + k/2 K1 and stage 2
+ *     forms acc = Psi + (T_A - Psi)/3 + k/3 K2 (= Psi + k/6 K1 + k/3 K2 in exact arithmetic),
+ *     14 field transfers per point-step.
  * 1 = TWO_KERNEL: the paper's single-storage scheme (`2d2shocs1/2`, `3d2shocs`):
  *     kernel A stores D = sum_d delta_d^2 Psi (D_b = lambda_b), kernel B applies step 2 +
  *     RHS + combine.  One more field of workspace (allocated on first use).
+ * 2 = FUSED_ACC16: as 0 but stage 1 stores acc = Psi + k/6 K1 explicitly (16 transfers per
+ *     point-step, the SURVEY §8(a) a6 form).
  * EINVAL for other values.                                                             */
 nlse2shoc_status nlse2shoc_set_variant(nlse2shoc_t, int variant);
 

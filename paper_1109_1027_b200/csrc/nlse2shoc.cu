@@ -331,7 +331,7 @@ static Field &stage_input(nlse2shoc_t H, Field &psi, int s) { return (s == 1 || 
 
 template <int DIMS, typename R, int MODE>
 static nlse2shoc_status launch_mode(nlse2shoc_t H, Field &psi, Field &in, StageParams<R> &P, cudaStream_t st) {
-  if (H->variant == 1) {
+  if (H->variant == 1) {  // two-kernel (stored D)
     TwoParams<R> Q;
     two_params<R>(H->dims, H->h, Q);
     return launch_two<DIMS, R>(0, MODE, reinterpret_cast<const cplx<R> *>(in.ptr),
@@ -350,12 +350,18 @@ static nlse2shoc_status launch_stage(nlse2shoc_t H, Field &psi, int s, double dt
   Field &in = stage_input(H, psi, s);
   cplx<R> *pPsi = reinterpret_cast<cplx<R> *>(psi.ptr), *pA = reinterpret_cast<cplx<R> *>(H->TA.ptr),
           *pB = reinterpret_cast<cplx<R> *>(H->TB.ptr), *pAcc = reinterpret_cast<cplx<R> *>(H->acc.ptr);
+  // reconstructed-accumulator form (14 transfers per point-step): fused 2D/3D variant 0
+  const bool recon = DIMS >= 2 && H->variant == 0;
   switch (s) {
     case 1:
       P.ca = R(dt / 6.0); P.cb = R(dt / 2.0); P.out_T = pA; P.out_acc = pAcc;
+      if constexpr (DIMS >= 2)
+        if (recon) return launch_stream<DIMS, R, M_S1R>(H, in, &psi.tm_pt, &H->acc.tm_pt, P, st);
       return launch_mode<DIMS, R, M_S1>(H, psi, in, P, st);
     case 2:
       P.ca = R(dt / 3.0); P.cb = R(dt / 2.0); P.out_T = pB; P.out_acc = pAcc;
+      if constexpr (DIMS >= 2)
+        if (recon) return launch_stream<DIMS, R, M_S2R>(H, in, &psi.tm_pt, &H->acc.tm_pt, P, st);
       return launch_mode<DIMS, R, M_S2>(H, psi, in, P, st);
     case 3:
       P.ca = R(dt / 3.0); P.cb = R(dt); P.out_T = pA; P.out_acc = pAcc;
@@ -801,7 +807,8 @@ size_t nlse2shoc_workspace_bytes(nlse2shoc_t H) {
 
 nlse2shoc_status nlse2shoc_set_variant(nlse2shoc_t H, int variant) {
   if (!H) return fail(NLSE2SHOC_EINVAL, "NULL handle");
-  if (variant != 0 && variant != 1) return fail(NLSE2SHOC_EINVAL, "variant must be 0 (fused) or 1 (two-kernel)");
+  if (variant < 0 || variant > 2)
+    return fail(NLSE2SHOC_EINVAL, "variant must be 0 (fused), 1 (two-kernel) or 2 (fused, 16-transfer accumulator)");
   for (nlse2shoc_t S : H->slabs) TRY(nlse2shoc_set_variant(S, variant));
   if (variant == 1 && H->slabs.empty()) TRY(ensure_D(H));
   H->variant = variant;

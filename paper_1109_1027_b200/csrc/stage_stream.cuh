@@ -30,7 +30,11 @@
 
 namespace nlse {
 
-enum Mode { M_S1 = 1, M_S2 = 2, M_S3 = 3, M_S4 = 4, M_LAP = 5 };
+// Stage kinds.  M_S1..M_S4: the four RK4 stages with the Psi-space accumulator (16 transfers
+// per point-step).  M_S1R / M_S2R: stages 1-2 of the reconstructed-accumulator form (14
+// transfers): stage 1 writes only T_A, stage 2 forms acc = Psi + (T_A - Psi)/3 + k/3 K2
+// ((T_A - Psi)/3 = k/6 K1 in exact arithmetic).  M_LAP: the Laplacian alone.
+enum Mode { M_S1 = 1, M_S2 = 2, M_S3 = 3, M_S4 = 4, M_LAP = 5, M_S1R = 6, M_S2R = 7 };
 
 // Tile configuration per (dims, precision).  W = smem row width in complex elements
 // (tile + 2+2 halo, rounded so that it splits into NBOX equal TMA boxes); every TMA
@@ -125,7 +129,12 @@ template <int DIMS, typename R> struct Layout {
   static_assert(C::NBOX == 1 || (BW * 8) % 128 == 0, "T sub-boxes 128-byte aligned");
   static_assert(C::NBOXP == 1 || (BWP * 8) % 128 == 0, "P sub-boxes 128-byte aligned");
   static_assert((C::TX / C::PPX) * (C::TY / C::RPW) == C::NCW * 32, "thread map");
-  template <int MODE> __host__ __device__ static constexpr bool needs_psi() { return MODE == M_S2 || MODE == M_S3; }
+  template <int MODE> __host__ __device__ static constexpr bool needs_psi() {
+    return MODE == M_S2 || MODE == M_S3 || MODE == M_S2R;
+  }
+  template <int MODE> __host__ __device__ static constexpr bool writes_acc() {
+    return MODE == M_S1 || MODE == M_S2 || MODE == M_S3 || MODE == M_S2R;
+  }
   template <int MODE> __host__ __device__ static constexpr bool needs_acc() { return MODE == M_S2 || MODE == M_S3 || MODE == M_S4; }
   template <int MODE> __host__ __device__ static constexpr int pa_tiles() { return (needs_psi<MODE>() ? 1 : 0) + (needs_acc<MODE>() ? 1 : 0); }
   template <int MODE> __host__ __device__ static constexpr int rt() {
@@ -396,7 +405,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
     int sp = int(pcnt % RPM);
     uint32_t php = (pcnt / RPM) & 1;
     cplx<R> *outT = P.out_T + int64_t(kb) * P.plane + int64_t(y0 + ly0) * P.pitch + (x0 + lx0);
-    cplx<R> *outA = (MODE != M_LAP && MODE != M_S4) ? P.out_acc + (outT - P.out_T) : nullptr;
+    cplx<R> *outA = (LY::template writes_acc<MODE>()) ? P.out_acc + (outT - P.out_T) : nullptr;
 
     // streamed-axis potential table, software-pipelined one plane ahead (its global load
     // would otherwise sit on the critical path of every plane)
@@ -545,6 +554,11 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
           } else if (MODE == M_S1) {
             oA[q] = iaxpy(c, ca, tF);
             oT[q] = iaxpy(c, cb, tF);
+          } else if (MODE == M_S1R) {
+            oT[q] = iaxpy(c, cb, tF);
+          } else if (MODE == M_S2R) {
+            oA[q] = iaxpy(axpy(psv[q], R(1.0 / 3.0), c - psv[q]), ca, tF);
+            oT[q] = iaxpy(psv[q], cb, tF);
           } else if (MODE == M_S2 || MODE == M_S3) {
             oA[q] = iaxpy(acv[q], ca, tF);
             oT[q] = iaxpy(psv[q], cb, tF);
@@ -558,19 +572,19 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
 #pragma unroll
         for (int q = 0; q < PPX; ++q) all = all && valid[q];
         cplx<R> *oTr = outT + int64_t(r) * P.pitch;
-        cplx<R> *oAr = (MODE != M_LAP && MODE != M_S4) ? outA + int64_t(r) * P.pitch : nullptr;
+        cplx<R> *oAr = (LY::template writes_acc<MODE>()) ? outA + int64_t(r) * P.pitch : nullptr;
         if (all) {
 #pragma unroll
           for (int v = 0; v < PPX / VV::CPV; ++v) {
             st_stream(reinterpret_cast<typename VV::T *>(oTr) + v, VV::join(oT + v * VV::CPV));
-            if (MODE != M_LAP && MODE != M_S4) st_stream(reinterpret_cast<typename VV::T *>(oAr) + v, VV::join(oA + v * VV::CPV));
+            if (LY::template writes_acc<MODE>()) st_stream(reinterpret_cast<typename VV::T *>(oAr) + v, VV::join(oA + v * VV::CPV));
           }
         } else {
 #pragma unroll
           for (int q = 0; q < PPX; ++q) {
             if (!valid[q]) continue;
             oTr[q] = oT[q];
-            if (MODE != M_LAP && MODE != M_S4) oAr[q] = oA[q];
+            if (LY::template writes_acc<MODE>()) oAr[q] = oA[q];
           }
         }
         // queue shift: (k-2, k-1, k+1) <- (k-1, k, k+2)
@@ -582,7 +596,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
         }
       }
       outT += P.plane;
-      if (MODE != M_LAP && MODE != M_S4) outA += P.plane;
+      if (LY::template writes_acc<MODE>()) outA += P.plane;
       __syncwarp();
       if (NPA) {
         if (lane == 0) mbar_arrive(&emptyP[sp]);
@@ -649,6 +663,11 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
           } else if (MODE == M_S1) {
             oA[q] = iaxpy(c, ca, tF);
             oT[q] = iaxpy(c, cb, tF);
+          } else if (MODE == M_S1R) {
+            oT[q] = iaxpy(c, cb, tF);
+          } else if (MODE == M_S2R) {
+            oA[q] = iaxpy(axpy(psv[q], R(1.0 / 3.0), c - psv[q]), ca, tF);
+            oT[q] = iaxpy(psv[q], cb, tF);
           } else if (MODE == M_S2 || MODE == M_S3) {
             oA[q] = iaxpy(acv[q], ca, tF);
             oT[q] = iaxpy(psv[q], cb, tF);
@@ -660,7 +679,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
 #pragma unroll
         for (int v = 0; v < PPX / VV::CPV; ++v) {
           st_stream(reinterpret_cast<typename VV::T *>(outT + r * pitch) + v, VV::join(oT + v * VV::CPV));
-          if (MODE != M_LAP && MODE != M_S4)
+          if (LY::template writes_acc<MODE>())
             st_stream(reinterpret_cast<typename VV::T *>(outA + r * pitch) + v, VV::join(oA + v * VV::CPV));
         }
 #pragma unroll
@@ -671,7 +690,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
         }
       }
       outT += plane;
-      if (MODE != M_LAP && MODE != M_S4) outA += plane;
+      if (LY::template writes_acc<MODE>()) outA += plane;
       __syncwarp();
       if (NPA) {
         if (lane == 0) mbar_arrive(&emptyP[sp]);

@@ -57,7 +57,7 @@ def test_laplacian_parity(dims, n, dtype, bc, V, variant):
     assert H.rel_l2(L.cpu().numpy(), Lo) <= tol
 
 
-@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("variant", [0, 1, 2])
 @pytest.mark.parametrize("dims,n,dtype,bc,V", CASES[::2])
 def test_rk4_parity_10_steps(dims, n, dtype, bc, V, variant):
     w = _small(dims, n, bc, dtype, V)
@@ -86,12 +86,13 @@ def test_fused_and_two_kernel_agree_3d():
     w = _small(3, (70, 35, 11), "dirichlet", "c128", "harmonic", aniso=False)
     psi = H.psi0_host(w, "c128")
     outs = []
-    for v in (0, 1):
+    for v in (0, 1, 2):
         S = H.gpu_solver(w, "c128", v)
         g = _dev(psi)
         S.rk4(g, 1e-4, 5)
         outs.append(g.cpu().numpy())
     assert H.rel_l2(outs[0], outs[1]) <= 1e-13
+    assert H.rel_l2(outs[0], outs[2]) <= 1e-13
 
 
 def test_edge_cases_and_errors():
