@@ -265,6 +265,8 @@ static nlse2shoc_status launch_stream(nlse2shoc_t H, Field &in, const CUtensorMa
     P.prog = H->prog;
     P.epoch = H->epoch;
     P.lead = lead;
+    static const int pair = getenv("NLSE_LEAD_PAIR") ? atoi(getenv("NLSE_LEAD_PAIR")) : 1;
+    P.lead_pair = pair;
   }
   const CUtensorMap *lo = P.has_lo_halo ? &in.tm_lo : &in.tm;
   const CUtensorMap *hi = P.has_hi_halo ? &in.tm_hi : &in.tm;

@@ -103,6 +103,7 @@ template <typename R> struct StageParams {
   uint32_t *prog;        // per-tile producer progress (epoch << 16 | planes issued), or null
   uint32_t epoch;        // launch tag of this stage's progress words
   int lead;              // max planes a tile's producer may run ahead of its neighbours
+  int lead_pair;         // couple only x-partner tiles (t, t^1) instead of all 4 neighbours
   uint32_t *rbar;        // round barrier counter (producers start each round together), or null
   cplx<R> *out_T;        // T_s (stages 1-3), psi^{n+1} (stage 4), L (laplacian mode)
   cplx<R> *out_acc;      // accumulator (stages 1-3)
@@ -250,7 +251,14 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
       }
       // stencil-input planes are re-read (halos) by neighbouring tiles: keep them in L2;
       // Psi^n / acc tiles are read exactly once: evict first.
-      const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
+#ifndef NLSE_TPOL
+#define NLSE_TPOL 2
+#endif
+#ifndef NLSE_PPOL
+#define NLSE_PPOL 0
+#endif
+      const uint64_t pol_keep = NLSE_TPOL == 2 ? policy_evict_last() : (NLSE_TPOL == 1 ? policy_evict_normal() : policy_evict_first());
+      const uint64_t pol_stream = NLSE_PPOL == 0 ? policy_evict_first() : policy_evict_normal();
       uint32_t tcnt = 0, pcnt = 0;
       for (int t = blockIdx.x; t < P.ntiles; t += G) {
         const int chunk = t / ncol, col = t % ncol;
@@ -269,10 +277,15 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
         int nb[4], nnb = 0;
         if (P.prog) {
           const int round = t / G, cx = col % P.ncx, cyy = col / P.ncx;
-          const int cand[4] = {cx > 0 ? t - 1 : -1, cx + 1 < P.ncx ? t + 1 : -1, cyy > 0 ? t - P.ncx : -1,
-                               cyy + 1 < P.ncy ? t + P.ncx : -1};
-          for (int i = 0; i < 4; ++i)
-            if (cand[i] >= 0 && cand[i] < P.ntiles && cand[i] / G == round) nb[nnb++] = cand[i];
+          if (P.lead_pair) {  // only the x-partner tile (t ^ 1), run by CTA blockIdx ^ 1
+            const int pt = t ^ 1;
+            if (pt < P.ntiles && pt / G == round && (pt % ncol) / P.ncx == cyy) nb[nnb++] = pt;
+          } else {
+            const int cand[4] = {cx > 0 ? t - 1 : -1, cx + 1 < P.ncx ? t + 1 : -1, cyy > 0 ? t - P.ncx : -1,
+                                 cyy + 1 < P.ncy ? t + P.ncx : -1};
+            for (int i = 0; i < 4; ++i)
+              if (cand[i] >= 0 && cand[i] < P.ntiles && cand[i] / G == round) nb[nnb++] = cand[i];
+          }
         }
         int issued = 0, seen = 0;  // planes issued for this tile; min neighbour progress seen
         auto gate = [&](int j) {

@@ -72,3 +72,17 @@ def test_loopback_C4_full_size_matches_single_gpu():
     S8.rk4(b, dt, 2)
     assert torch.equal(torch.view_as_real(a), torch.view_as_real(b))
     S8.close()
+
+
+def test_nccl_sharded_handle_single_rank():
+    """The real NCCL path: a one-rank communicator (no neighbours, so no exchange) must give
+    exactly the single-GPU result; exercises ncclGetUniqueId / ncclCommInitRank."""
+    import paper_1109_1027_b200 as nl
+
+    w = configs.SMALL(3, (40, 33, 31), "dirichlet", dtype="c64", V="harmonic", noise=0.05)
+    psi0 = H.psi0_host(w, "c64")
+    ref, _ = _run(w, "c64", None, 0, 4, 1e-4, psi0)
+    uid = nl.nlse2shoc_get_unique_id()
+    assert len(uid) == 128
+    got, _ = _run(w, "c64", {"uid": uid, "rank": 0, "nranks": 1}, 0, 4, 1e-4, psi0)
+    assert np.array_equal(got.view(np.uint8), ref.view(np.uint8))
