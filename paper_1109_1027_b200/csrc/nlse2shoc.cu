@@ -416,7 +416,34 @@ static nlse2shoc_status exchange(View &v, int s, cudaStream_t st) {
   return NLSE2SHOC_OK;
 }
 
+// Small 1D grids: one resident CTA runs the whole call (stage_line.cuh).
+template <typename R> static nlse2shoc_status rk4_resident_1d(nlse2shoc_t H, Field &psi, double dt, int64_t nsteps,
+                                                              cudaStream_t st) {
+  StageParams<R> P;
+  fill_params<R>(H, P);
+  const size_t smem = size_t(4) * size_t(H->nx) * sizeof(cplx<R>);
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(resident_line_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  resident_line_kernel<R><<<1, 1024, smem, st>>>(reinterpret_cast<cplx<R> *>(psi.ptr), nsteps, R(dt), P);
+  CUDA_TRY(cudaGetLastError());
+  ++H->launches;
+  return NLSE2SHOC_OK;
+}
+
+static bool resident_ok(nlse2shoc_t H) {
+  return H->dims == 1 && H->slabs.empty() && !H->sharded && H->variant != 1 &&
+         size_t(4) * size_t(H->nx) * H->S <= size_t(200) * 1024 && !getenv("NLSE_NO_RESIDENT");
+}
+
 static nlse2shoc_status run_rk4(View &v, double dt, int64_t nsteps, cudaStream_t st) {
+  if (v.hs.size() == 1 && resident_ok(v.hs[0])) {
+    nlse2shoc_t H = v.hs[0];
+    return H->dtype == NLSE2SHOC_C64 ? rk4_resident_1d<float>(H, v.psis[0], dt, nsteps, st)
+                                     : rk4_resident_1d<double>(H, v.psis[0], dt, nsteps, st);
+  }
   for (int64_t n = 0; n < nsteps; ++n)
     for (int s = 1; s <= 4; ++s) {
       TRY(exchange(v, s, st));

@@ -9,42 +9,95 @@
 
 namespace nlse {
 
+// One point of the 1D stage: returns t with F = i t (and L for the Laplacian output).
+template <typename R>
+__device__ __forceinline__ cplx<R> line_point(const cplx<R> *__restrict__ Tin, int64_t i, int n, const StageParams<R> &P,
+                                             cplx<R> &c, cplx<R> &L) {
+  using CT = cplx<R>;
+  c = Tin[i];
+  const bool bnd = i == 0 || i == n - 1;
+  const R V = potential(P, int(i), 0, 0);
+  const R N = fma(P.s, norm2(c), -V);
+  if (!bnd) {
+    const CT m1 = Tin[i - 1], p1 = Tin[i + 1];
+    CT m2, p2;
+    if (i >= 2) m2 = Tin[i - 2];
+    else m2 = axpy(R(2) * m1 - c, P.hx2, lambda_b(P, m1, potential(P, 0, 0, 0)));
+    if (i <= n - 3) p2 = Tin[i + 2];
+    else p2 = axpy(R(2) * p1 - c, P.hx2, lambda_b(P, p1, potential(P, n - 1, 0, 0)));
+    L = P.cx * (R(16) * (m1 + p1) - (m2 + p2) - R(30) * c);
+    return axpy(N * c, P.a, L);  // a L + N c
+  }
+  L = lambda_b(P, c, V);
+  return P.bc == 0 ? mk<R>(R(0), R(0)) : N * c;
+}
+
 template <typename R, int MODE>
 __global__ void __launch_bounds__(256) stage_line_kernel(const cplx<R> *__restrict__ Tin, const cplx<R> *__restrict__ psi,
                                                          const cplx<R> *__restrict__ acc, const StageParams<R> P) {
   using CT = cplx<R>;
   const int n = P.nx;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    const CT c = Tin[i];
-    const bool bnd = i == 0 || i == n - 1;
-    const R V = potential(P, int(i), 0, 0);
-    const R N = fma(P.s, norm2(c), -V);
-    CT L, F;
-    if (!bnd) {
-      const CT m1 = Tin[i - 1], p1 = Tin[i + 1];
-      CT m2, p2;
-      if (i >= 2) m2 = Tin[i - 2];
-      else m2 = axpy(R(2) * m1 - c, P.hx2, lambda_b(P, m1, potential(P, 0, 0, 0)));
-      if (i <= n - 3) p2 = Tin[i + 2];
-      else p2 = axpy(R(2) * p1 - c, P.hx2, lambda_b(P, p1, potential(P, n - 1, 0, 0)));
-      L = P.cx * (R(16) * (m1 + p1) - (m2 + p2) - R(30) * c);
-      F = mk<R>(-fma(P.a, L.im, N * c.im), fma(P.a, L.re, N * c.re));
-    } else {
-      L = lambda_b(P, c, V);
-      F = P.bc == 0 ? mk<R>(R(0), R(0)) : mk<R>(-(N * c.im), N * c.re);
-    }
+    CT c, L;
+    const CT t = line_point(Tin, i, n, P, c, L);
     if (MODE == M_LAP) {
       P.out_T[i] = L;
     } else if (MODE == M_S1) {
-      P.out_acc[i] = axpy(c, P.ca, F);
-      P.out_T[i] = axpy(c, P.cb, F);
+      P.out_acc[i] = iaxpy(c, P.ca, t);
+      P.out_T[i] = iaxpy(c, P.cb, t);
     } else if (MODE == M_S2 || MODE == M_S3) {
-      P.out_acc[i] = axpy(acc[i], P.ca, F);
-      P.out_T[i] = axpy(psi[i], P.cb, F);
+      P.out_acc[i] = iaxpy(acc[i], P.ca, t);
+      P.out_T[i] = iaxpy(psi[i], P.cb, t);
     } else {
-      P.out_T[i] = axpy(acc[i], P.cb, F);
+      P.out_T[i] = iaxpy(acc[i], P.cb, t);
     }
   }
+}
+
+// Resident small-grid 1D solver: the whole grid (Psi, T_A, T_B, acc) lives in one CTA's
+// shared memory and the CTA runs all nsteps x 4 stages of an nlse2shoc_rk4 call, separated
+// by barriers.  Same per-point arithmetic as stage_line_kernel; one launch per call instead
+// of 4 per step (C1: 2000 steps on 1024 points is otherwise launch-latency bound).
+template <typename R>
+__global__ void __launch_bounds__(1024, 1) resident_line_kernel(cplx<R> *__restrict__ psi_g, int64_t nsteps, R dt,
+                                                                const StageParams<R> P) {
+  using CT = cplx<R>;
+  extern __shared__ __align__(16) unsigned char rsm[];
+  const int n = P.nx;
+  CT *psi = reinterpret_cast<CT *>(rsm), *TA = psi + n, *TB = TA + n, *acc = TB + n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) psi[i] = psi_g[i];
+  __syncthreads();
+  const R c6 = dt / R(6), c3 = dt / R(3), c2 = dt / R(2);
+  for (int64_t step = 0; step < nsteps; ++step) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {  // stage 1
+      CT c, L;
+      const CT t = line_point<R>(psi, i, n, P, c, L);
+      acc[i] = iaxpy(c, c6, t);
+      TA[i] = iaxpy(c, c2, t);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {  // stage 2
+      CT c, L;
+      const CT t = line_point<R>(TA, i, n, P, c, L);
+      acc[i] = iaxpy(acc[i], c3, t);
+      TB[i] = iaxpy(psi[i], c2, t);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {  // stage 3
+      CT c, L;
+      const CT t = line_point<R>(TB, i, n, P, c, L);
+      acc[i] = iaxpy(acc[i], c3, t);
+      TA[i] = iaxpy(psi[i], dt, t);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {  // stage 4
+      CT c, L;
+      const CT t = line_point<R>(TA, i, n, P, c, L);
+      psi[i] = iaxpy(acc[i], c6, t);
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) psi_g[i] = psi[i];
 }
 
 // ---------------------------------------------------------------------------------------
