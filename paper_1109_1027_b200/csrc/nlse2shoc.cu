@@ -234,7 +234,7 @@ static nlse2shoc_status launch_stream(nlse2shoc_t H, Field &in, const CUtensorMa
   // z-chunks: minimise rounds * (chunk length + priming cost)
   int best = 1;
   double bestc = 1e300;
-  for (int nc = 1; nc <= 16 && nc <= H->nz; ++nc) {
+  for (int nc = 1; nc <= 256 && 4 * nc <= H->nz + 3; ++nc) {
     const double rounds = std::ceil(double(ncol) * nc / G0);
     const double len = std::ceil(double(H->nz) / nc) + 1.5;
     const double c = rounds * len;

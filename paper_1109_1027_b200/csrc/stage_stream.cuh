@@ -72,6 +72,20 @@ template <> struct Cfg<3, float> : Rings<68 * (NLSE3F_TY + 4) * 8, 64 * NLSE3F_T
 template <> struct Cfg<3, double> : Rings<36 * (28 + 4) * 16, 32 * 28 * 16> {
   static constexpr int TX = 32, TY = 28, PPX = 1, RPW = 2, NCW = 14, NBOX = 1, NBOXP = 1, W = 36;
 };
+// 2D: the streamed axis is y and a "plane" is one row of TX + halo; 4 x-points per thread so
+// the per-row pipeline overhead is amortised (1040-wide slots split into 128-byte-aligned
+// TMA boxes of 208 eight-byte elements).
+#ifndef NLSE2D_PPX
+#define NLSE2D_PPX 1
+#endif
+#if NLSE2D_PPX == 4
+template <> struct Cfg<2, float> : Rings<1040 * 8, 1024 * 8> {
+  static constexpr int TX = 1024, TY = 1, PPX = 4, RPW = 1, NCW = 8, NBOX = 5, NBOXP = 4, W = 1040;
+};
+template <> struct Cfg<2, double> : Rings<1040 * 16, 1024 * 16> {
+  static constexpr int TX = 1024, TY = 1, PPX = 4, RPW = 1, NCW = 8, NBOX = 10, NBOXP = 8, W = 1040;
+};
+#else
 template <> struct Cfg<2, float> {
   static constexpr int TX = 512, TY = 1, PPX = 2, RPW = 1, NCW = 8, NBOX = 3, NBOXP = 2, W = 528;
   static constexpr int RT0 = 40, RT1 = 24, RP1 = 20, RT2 = 20, RP2 = 12;
@@ -80,6 +94,7 @@ template <> struct Cfg<2, double> {
   static constexpr int TX = 256, TY = 1, PPX = 1, RPW = 1, NCW = 8, NBOX = 3, NBOXP = 2, W = 264;
   static constexpr int RT0 = 40, RT1 = 24, RP1 = 20, RT2 = 20, RP2 = 12;
 };
+#endif
 
 template <typename R> struct StageParams {
   int nx, ny, nz;        // local extents: x, y (1 in 2D), streamed axis (local slab)
