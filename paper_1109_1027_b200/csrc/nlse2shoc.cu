@@ -352,18 +352,22 @@ static nlse2shoc_status launch_stage(nlse2shoc_t H, Field &psi, int s, double dt
   Field &in = stage_input(H, psi, s);
   cplx<R> *pPsi = reinterpret_cast<cplx<R> *>(psi.ptr), *pA = reinterpret_cast<cplx<R> *>(H->TA.ptr),
           *pB = reinterpret_cast<cplx<R> *>(H->TB.ptr), *pAcc = reinterpret_cast<cplx<R> *>(H->acc.ptr);
-  // reconstructed-accumulator form (14 transfers per point-step): fused 2D/3D variant 0
-  const bool recon = DIMS >= 2 && H->variant == 0;
+  // reconstructed-accumulator form (14 transfers per point-step): fused variant 0
+  const bool recon = H->variant == 0;
   switch (s) {
     case 1:
       P.ca = R(dt / 6.0); P.cb = R(dt / 2.0); P.out_T = pA; P.out_acc = pAcc;
-      if constexpr (DIMS >= 2)
-        if (recon) return launch_stream<DIMS, R, M_S1R>(H, in, &psi.tm_pt, &H->acc.tm_pt, P, st);
+      if (recon) {
+        if constexpr (DIMS >= 2) return launch_stream<DIMS, R, M_S1R>(H, in, &psi.tm_pt, &H->acc.tm_pt, P, st);
+        else return launch_line<R, M_S1R>(H, in.ptr, psi.ptr, H->acc.ptr, P, st);
+      }
       return launch_mode<DIMS, R, M_S1>(H, psi, in, P, st);
     case 2:
       P.ca = R(dt / 3.0); P.cb = R(dt / 2.0); P.out_T = pB; P.out_acc = pAcc;
-      if constexpr (DIMS >= 2)
-        if (recon) return launch_stream<DIMS, R, M_S2R>(H, in, &psi.tm_pt, &H->acc.tm_pt, P, st);
+      if (recon) {
+        if constexpr (DIMS >= 2) return launch_stream<DIMS, R, M_S2R>(H, in, &psi.tm_pt, &H->acc.tm_pt, P, st);
+        else return launch_line<R, M_S2R>(H, in.ptr, psi.ptr, H->acc.ptr, P, st);
+      }
       return launch_mode<DIMS, R, M_S2>(H, psi, in, P, st);
     case 3:
       P.ca = R(dt / 3.0); P.cb = R(dt); P.out_T = pA; P.out_acc = pAcc;

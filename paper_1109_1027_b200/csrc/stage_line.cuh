@@ -45,6 +45,12 @@ __global__ void __launch_bounds__(256) stage_line_kernel(const cplx<R> *__restri
     } else if (MODE == M_S1) {
       P.out_acc[i] = iaxpy(c, P.ca, t);
       P.out_T[i] = iaxpy(c, P.cb, t);
+    } else if (MODE == M_S1R) {
+      P.out_T[i] = iaxpy(c, P.cb, t);
+    } else if (MODE == M_S2R) {
+      const CT ps = psi[i];
+      P.out_acc[i] = iaxpy(axpy(ps, R(1.0 / 3.0), c - ps), P.ca, t);
+      P.out_T[i] = iaxpy(ps, P.cb, t);
     } else if (MODE == M_S2 || MODE == M_S3) {
       P.out_acc[i] = iaxpy(acc[i], P.ca, t);
       P.out_T[i] = iaxpy(psi[i], P.cb, t);

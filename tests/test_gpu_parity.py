@@ -234,3 +234,20 @@ def test_C5W_full_size_crops(dtype):
     w = configs.C5W(1)
     T = [([0, 0, 0], [20, 20, 20]), ([380, 370, 90], [30, 30, 12]), ([748, 750, 176], [20, 18, 16])]
     _crop_parity(w, dtype, 2, T, H.TOL[dtype])
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_1d_multilaunch_path_small_grid(dtype, monkeypatch):
+    """Small 1D grids normally run on the resident single-CTA solver; force the per-stage
+    launch path (used for large 1D grids such as C2) and check parity on a small grid."""
+    monkeypatch.setenv("NLSE_NO_RESIDENT", "1")
+    w = _small(1, (1001,), "dirichlet", dtype, "harmonic")
+    S = H.gpu_solver(w, dtype)
+    psi = H.psi0_host(w, dtype)
+    P = H.oracle_problem(w)
+    dt = 0.8 * oracle.kmax(P, psi.astype(np.complex128))
+    g = _dev(psi)
+    S.rk4(g, dt, 10)
+    assert S.last_launch_count == 40
+    ref = oracle.rk4(P, psi.astype(np.complex128), dt, 10)
+    assert H.rel_l2(g.cpu().numpy(), ref) <= H.TOL[dtype]
