@@ -371,9 +371,17 @@ static nlse2shoc_status launch_stage(nlse2shoc_t H, Field &psi, int s, double dt
       return launch_mode<DIMS, R, M_S2>(H, psi, in, P, st);
     case 3:
       P.ca = R(dt / 3.0); P.cb = R(dt); P.out_T = pA; P.out_acc = pAcc;
+      if (recon) {
+        if constexpr (DIMS >= 2) return launch_stream<DIMS, R, M_S3R>(H, in, &psi.tm_pt, &H->acc.tm_pt, P, st);
+        else return launch_line<R, M_S3R>(H, in.ptr, psi.ptr, H->acc.ptr, P, st);
+      }
       return launch_mode<DIMS, R, M_S3>(H, psi, in, P, st);
     case 4:
       P.ca = R(0); P.cb = R(dt / 6.0); P.out_T = pPsi; P.out_acc = nullptr;
+      if (recon) {
+        if constexpr (DIMS >= 2) return launch_stream<DIMS, R, M_S4R>(H, in, &psi.tm_pt, &H->acc.tm_pt, P, st);
+        else return launch_line<R, M_S4R>(H, in.ptr, psi.ptr, H->acc.ptr, P, st);
+      }
       return launch_mode<DIMS, R, M_S4>(H, psi, in, P, st);
     default:
       P.out_T = reinterpret_cast<cplx<R> *>(L);

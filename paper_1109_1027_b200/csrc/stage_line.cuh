@@ -51,6 +51,10 @@ __global__ void __launch_bounds__(256) stage_line_kernel(const cplx<R> *__restri
       const CT ps = psi[i];
       P.out_acc[i] = iaxpy(axpy(ps, R(1.0 / 3.0), c - ps), P.ca, t);
       P.out_T[i] = iaxpy(ps, P.cb, t);
+    } else if (MODE == M_S3R) {
+      P.out_T[i] = iaxpy(psi[i], P.cb, t);
+    } else if (MODE == M_S4R) {
+      P.out_T[i] = iaxpy(axpy(acc[i], R(1.0 / 3.0), c - psi[i]), P.cb, t);
     } else if (MODE == M_S2 || MODE == M_S3) {
       P.out_acc[i] = iaxpy(acc[i], P.ca, t);
       P.out_T[i] = iaxpy(psi[i], P.cb, t);

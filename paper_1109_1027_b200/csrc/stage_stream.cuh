@@ -34,7 +34,9 @@ namespace nlse {
 // per point-step).  M_S1R / M_S2R: stages 1-2 of the reconstructed-accumulator form (14
 // transfers): stage 1 writes only T_A, stage 2 forms acc = Psi + (T_A - Psi)/3 + k/3 K2
 // ((T_A - Psi)/3 = k/6 K1 in exact arithmetic).  M_LAP: the Laplacian alone.
-enum Mode { M_S1 = 1, M_S2 = 2, M_S3 = 3, M_S4 = 4, M_LAP = 5, M_S1R = 6, M_S2R = 7 };
+// M_S3R / M_S4R: stage 3 stores only T_A = Psi + k K3 and stage 4 forms
+// Psi' = acc + (T_A - Psi)/3 + k/6 K4 ((T_A - Psi)/3 = k/3 K3): 13 transfers in all.
+enum Mode { M_S1 = 1, M_S2 = 2, M_S3 = 3, M_S4 = 4, M_LAP = 5, M_S1R = 6, M_S2R = 7, M_S3R = 8, M_S4R = 9 };
 
 // Tile configuration per (dims, precision).  W = smem row width in complex elements
 // (tile + 2+2 halo, rounded so that it splits into NBOX equal TMA boxes); every TMA
@@ -146,12 +148,14 @@ template <int DIMS, typename R> struct Layout {
   static_assert(C::NBOXP == 1 || (BWP * 8) % 128 == 0, "P sub-boxes 128-byte aligned");
   static_assert((C::TX / C::PPX) * (C::TY / C::RPW) == C::NCW * 32, "thread map");
   template <int MODE> __host__ __device__ static constexpr bool needs_psi() {
-    return MODE == M_S2 || MODE == M_S3 || MODE == M_S2R;
+    return MODE == M_S2 || MODE == M_S3 || MODE == M_S2R || MODE == M_S3R || MODE == M_S4R;
   }
   template <int MODE> __host__ __device__ static constexpr bool writes_acc() {
     return MODE == M_S1 || MODE == M_S2 || MODE == M_S3 || MODE == M_S2R;
   }
-  template <int MODE> __host__ __device__ static constexpr bool needs_acc() { return MODE == M_S2 || MODE == M_S3 || MODE == M_S4; }
+  template <int MODE> __host__ __device__ static constexpr bool needs_acc() {
+    return MODE == M_S2 || MODE == M_S3 || MODE == M_S4 || MODE == M_S4R;
+  }
   template <int MODE> __host__ __device__ static constexpr int pa_tiles() { return (needs_psi<MODE>() ? 1 : 0) + (needs_acc<MODE>() ? 1 : 0); }
   template <int MODE> __host__ __device__ static constexpr int rt() {
     return pa_tiles<MODE>() == 0 ? C::RT0 : (pa_tiles<MODE>() == 1 ? C::RT1 : C::RT2);
@@ -587,6 +591,10 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
           } else if (MODE == M_S2R) {
             oA[q] = iaxpy(axpy(psv[q], R(1.0 / 3.0), c - psv[q]), ca, tF);
             oT[q] = iaxpy(psv[q], cb, tF);
+          } else if (MODE == M_S3R) {
+            oT[q] = iaxpy(psv[q], cb, tF);
+          } else if (MODE == M_S4R) {
+            oT[q] = iaxpy(axpy(acv[q], R(1.0 / 3.0), c - psv[q]), cb, tF);
           } else if (MODE == M_S2 || MODE == M_S3) {
             oA[q] = iaxpy(acv[q], ca, tF);
             oT[q] = iaxpy(psv[q], cb, tF);
@@ -696,6 +704,10 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
           } else if (MODE == M_S2R) {
             oA[q] = iaxpy(axpy(psv[q], R(1.0 / 3.0), c - psv[q]), ca, tF);
             oT[q] = iaxpy(psv[q], cb, tF);
+          } else if (MODE == M_S3R) {
+            oT[q] = iaxpy(psv[q], cb, tF);
+          } else if (MODE == M_S4R) {
+            oT[q] = iaxpy(axpy(acv[q], R(1.0 / 3.0), c - psv[q]), cb, tF);
           } else if (MODE == M_S2 || MODE == M_S3) {
             oA[q] = iaxpy(acv[q], ca, tF);
             oT[q] = iaxpy(psv[q], cb, tF);
