@@ -251,3 +251,33 @@ def test_1d_multilaunch_path_small_grid(dtype, monkeypatch):
     assert S.last_launch_count == 40
     ref = oracle.rk4(P, psi.astype(np.complex128), dt, 10)
     assert H.rel_l2(g.cpu().numpy(), ref) <= H.TOL[dtype]
+
+
+def _core_box_work(w, lo, cnt):
+    """The workload restricted to a box treated as its own Dirichlet domain (same h, V,
+    seeded Psi0 values of that region of the global grid)."""
+    import copy
+
+    g = w["grid"]
+    wc = copy.deepcopy(w)
+    wc["grid"] = {"dims": g["dims"], "n": list(cnt), "xmin": [g["xmin"][d] + lo[d] * g["h"][d] for d in range(3)],
+                  "h": list(g["h"])}
+    return wc
+
+
+@pytest.mark.parametrize("dtype,variant", [("c64", 0), ("c64", 2), ("c128", 0)])
+def test_C4_core_box_full_step_count(dtype, variant):
+    """C4 at its stated step count (100) on a 96^3 box around the ring core with C4's own
+    spacing (SURVEY A7 analogue): the whole-field parity the north star states, for the
+    default 13-transfer form and the explicit-accumulator form."""
+    w = configs.C4()
+    lo, cnt = [336, 336, 336], [96, 96, 96]
+    wc = _core_box_work(w, lo, cnt)
+    psi = H.psi0_host(w, dtype, lo, cnt)
+    P = oracle.problem_from_work(wc)
+    dt = 0.8 * oracle.kmax(P, psi.astype(np.complex128))
+    S = H.gpu_solver(wc, dtype, variant)
+    g = _dev(psi)
+    S.rk4(g, dt, w["steps"])
+    ref = oracle.rk4(P, psi.astype(np.complex128), dt, w["steps"])
+    assert H.rel_l2(g.cpu().numpy(), ref) <= H.TOL[dtype]
