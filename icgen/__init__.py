@@ -18,6 +18,7 @@ _SO = os.path.join(_HERE, "libicgen.so")
 
 ICG_NOISE, ICG_BRIGHT_SECH, ICG_DARK_TANH, ICG_TF_VORTEX2D = 0, 1, 2, 3
 ICG_TF_RING3D, ICG_GAUSS_NOISE, ICG_GAUSS_EXACT, ICG_SMOOTH_NOISE = 4, 5, 6, 7
+ICG_DARK_MOVING = 8
 
 
 class _Spec(ctypes.Structure):

@@ -13,7 +13,7 @@ from __future__ import annotations
 
 import copy
 
-from . import (ICG_BRIGHT_SECH, ICG_DARK_TANH, ICG_GAUSS_EXACT, ICG_GAUSS_NOISE,
+from . import (ICG_BRIGHT_SECH, ICG_DARK_MOVING, ICG_DARK_TANH, ICG_GAUSS_EXACT, ICG_GAUSS_NOISE,
                ICG_NOISE, ICG_SMOOTH_NOISE, ICG_TF_RING3D, ICG_TF_VORTEX2D)
 
 DIRICHLET, LAPZERO = "dirichlet", "lapzero"
@@ -108,6 +108,17 @@ def EXP_GAUSS(dims, h, t_end=10.0):
     steps = int(round(t_end / k))
     return _w(f"EXP{dims}_gauss_h{h}", g, 1.0, 0.0, V_harm(1.0, dims), DIRICHLET, steps,
               ["c128"], ("fixed", k), {"kind": ICG_GAUSS_EXACT, "p": [1.0, float(dims), 0.0]})
+
+
+def EXP_DARK(h, lo=-25.5, hi=31.0, t_end=10.0):
+    """PAPER.md Exp. 1: co-moving dark soliton `1dmds` with s = -1, a = 1,
+    c = 0.5, Omega = -1, MSD boundary, k = 5e-4, t = 10.  Domain: reading R5 ([-25.5, 31];
+    the paper says only 'large enough')."""
+    n = int(round((hi - lo) / h)) + 1
+    g = grid_inclusive([lo], [hi], [n])
+    k = 5e-4
+    return _w(f"EXP1_dark_h{h}", g, 1.0, -1.0, V_NONE, "msd", int(round(t_end / k)), ["c128"], ("fixed", k),
+              {"kind": ICG_DARK_MOVING, "p": [0.5, -1.0, 1.0, -1.0, 0.0]})
 
 
 def SMALL(dims, n, bc, dtype="c128", V="harmonic", noise=1e-2, seed=7, a=0.7, s=-0.9,

@@ -87,6 +87,13 @@ static void eval_point(const icg_spec *s, int64_t i, int64_t j, int64_t k, doubl
     r = amp * cos(ph) + p[0] * (2.0 * icg_uniform(s->seed, 1, gidx) - 1.0);
     m = amp * sin(ph) + p[0] * (2.0 * icg_uniform(s->seed, 2, gidx) - 1.0);
   } break;
+  case ICG_DARK_MOVING: {
+    const double c = p[0], Om = p[1], a = p[2], sn = p[3], t = p[4];
+    const double amp = sqrt(Om / sn) * tanh(sqrt(fabs(Om) / (2.0 * a)) * (x - c * t));
+    const double ph = (c / (2.0 * a)) * x + (Om - c * c / (4.0 * a)) * t;
+    r = amp * cos(ph);
+    m = amp * sin(ph);
+  } break;
   default:
     r = NAN; m = NAN;
   }

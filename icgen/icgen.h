@@ -32,9 +32,12 @@ enum icg_kind {
   ICG_GAUSS_NOISE = 5,  /* exp(-r^2/p0) + p1*noise                              (C5)   */
   ICG_GAUSS_EXACT = 6,  /* exp(-r^2/(2 p0)) * exp(-i p1 t), t = p2  (PAPER 2dexpsol /
                            3dexpsol; p1 = dims)                  */
-  ICG_SMOOTH_NOISE = 7  /* smooth analytic field + p0*noise at all points (tests):
+  ICG_SMOOTH_NOISE = 7, /* smooth analytic field + p0*noise at all points (tests):
                            (1+0.3 sin(x+0.5y-0.7z)) exp(i(0.8x - 0.6y + 0.4z))
                            * exp(-p1 r^2)                                              */
+  ICG_DARK_MOVING = 8   /* co-moving dark soliton (`1dmds`) at time p4:
+                           sqrt(Om/s) tanh(sqrt(|Om|/(2a)) (x - c t))
+                           * exp(i[(c/(2a)) x + (Om - c^2/(4a)) t]);  p0=c, p1=Om, p2=a, p3=s */
 };
 
 typedef struct {

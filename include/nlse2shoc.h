@@ -54,7 +54,11 @@ typedef enum {
  *             (reading R9).
  * At a d-face point b (index_d in {0, N_d-1}, all other indices interior) the per-axis
  * intermediate is D_d(b) = lambda_b - sum_{e != d} delta_e^2 Psi_b (reading R8).          */
-typedef enum { NLSE2SHOC_BC_DIRICHLET = 0, NLSE2SHOC_BC_LAPZERO = 1 } nlse2shoc_bc;
+/*  MSD:       modulus-squared Dirichlet, 1D only (EUNSUPPORTED otherwise):
+ *             lambda_b = [Re(D_{b-1}/Psi_{b-1}) + (N_{b-1} - N_b)/a] Psi_b (`msdbc_lap`, reading
+ *             R28), Psi_t,b = i Im(Psi_t,b-1 / Psi_b-1) Psi_b (`msdbc_ut`).  The stability bound
+ *             omits Table 1's MSD B term.                                                     */
+typedef enum { NLSE2SHOC_BC_DIRICHLET = 0, NLSE2SHOC_BC_LAPZERO = 1, NLSE2SHOC_BC_MSD = 2 } nlse2shoc_bc;
 
 typedef enum { NLSE2SHOC_C64 = 0, NLSE2SHOC_C128 = 1 } nlse2shoc_dtype;
 

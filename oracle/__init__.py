@@ -26,7 +26,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared", "-std=c11"]
 
-BC = {"dirichlet": 0, "lapzero": 1}
+BC = {"dirichlet": 0, "lapzero": 1, "msd": 2}
 SCHEME = {"2shoc": 0, "cd": 1}
 
 

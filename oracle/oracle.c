@@ -21,6 +21,7 @@ static geom mk_geom(const orc_problem *P) {
 
 static int valid(const orc_problem *P) {
   if (!P || P->dims < 1 || P->dims > 3 || !(P->a > 0.0)) return 0;
+  if (P->bc == ORC_BC_MSD && P->dims != 1) return 0; /* MSD: 1D only (reading R28) */
   for (int d = 0; d < P->dims; ++d)
     if (P->n[d] < 5 || !(P->h[d] > 0.0)) return 0;
   return 1;
@@ -109,6 +110,15 @@ static void lap_core(const orc_problem *P, const double *psi, double *L, double 
         if (P->bc == ORC_BC_DIRICHLET) {
           lr = -(N[p] * psi[2 * p]) / P->a;
           li = -(N[p] * psi[2 * p + 1]) / P->a;
+        } else if (P->bc == ORC_BC_MSD) {
+          /* `msdbc_lap`: Lap_b = [Im(i Lap_{b-1} / Psi_{b-1}) + (N_{b-1} - N_b)/a] Psi_b,
+           * Im(i z) = Re(z), with Lap_{b-1} the step-1 value D_{b-1} (reading R28).        */
+          const int64_t q = (i == 0) ? p + 1 : p - 1;
+          const double pr = psi[2 * q], pi = psi[2 * q + 1];
+          const double re_ratio = (D[d][2 * q] * pr + D[d][2 * q + 1] * pi) / (pr * pr + pi * pi);
+          const double fac = re_ratio + (N[q] - N[p]) / P->a;
+          lr = fac * psi[2 * p];
+          li = fac * psi[2 * p + 1];
         }
         for (int e = 0; e < dims; ++e) {
           if (e == d) continue;
@@ -129,6 +139,9 @@ static void lap_core(const orc_problem *P, const double *psi, double *L, double 
       if (P->bc == ORC_BC_DIRICHLET) {
         L[2 * p] = -(N[p] * psi[2 * p]) / P->a;
         L[2 * p + 1] = -(N[p] * psi[2 * p + 1]) / P->a;
+      } else if (P->bc == ORC_BC_MSD) { /* 1D: the face value filled above */
+        L[2 * p] = D[0][2 * p];
+        L[2 * p + 1] = D[0][2 * p + 1];
       } else {
         L[2 * p] = 0.0;
         L[2 * p + 1] = 0.0;
@@ -204,6 +217,18 @@ static void rhs_core(const orc_problem *P, const double *psi, double *F, scratch
       F[2 * p + 1] = xr;
     }
   })
+  if (P->bc == ORC_BC_MSD) {
+    /* `msdbc_ut`: Psi_t,b = i Im(Psi_t,b-1 / Psi_b-1) Psi_b, after the interior. */
+    const int64_t n = g.n[0];
+    const int64_t bs[2] = {0, n - 1}, qs[2] = {1, n - 2};
+    for (int k = 0; k < 2; ++k) {
+      const int64_t b = bs[k], q = qs[k];
+      const double pr = psi[2 * q], pi = psi[2 * q + 1];
+      const double m = (F[2 * q + 1] * pr - F[2 * q] * pi) / (pr * pr + pi * pi);
+      F[2 * b] = -(m * psi[2 * b + 1]);
+      F[2 * b + 1] = m * psi[2 * b];
+    }
+  }
 }
 
 int orc_rhs(const orc_problem *P, const double *psi, double *F) {

@@ -18,6 +18,8 @@
  *     Lap_b  = lambda_b
  *   Psi_t boundary:  F_b = 0 (Dirichlet, `dbc_ut`);  F_b = i N_b Psi_b
  *     (Laplacian-zero, reading R9)
+ *   MSD (1D only): lambda_b = [Re(D_{b-1}/Psi_{b-1}) + (N_{b-1}-N_b)/a] Psi_b
+ *     (`msdbc_lap`, reading R28); F_b = i Im(F_{b-1}/Psi_{b-1}) Psi_b (`msdbc_ut`)
  *   RK4 exactly as the paper's 10-step listing with K_tot, K_tmp, Psi_tmp (`RK4`,
  *     P:366-382).
  *   CD scheme (RK4+CD): Lap = sum_d D_d, same boundary values.
@@ -33,7 +35,7 @@
 extern "C" {
 #endif
 
-enum { ORC_BC_DIRICHLET = 0, ORC_BC_LAPZERO = 1 };
+enum { ORC_BC_DIRICHLET = 0, ORC_BC_LAPZERO = 1, ORC_BC_MSD = 2 };
 enum { ORC_SCHEME_2SHOC = 0, ORC_SCHEME_CD = 1 };
 
 typedef struct {

@@ -12,7 +12,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.environ.get("NLSE_LIB") or os.path.join(_HERE, "libnlse2shoc.so")
 
 OK, EINVAL, ENOMEM, ECUDA, ENCCL, ENONFINITE, EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
-BC = {"dirichlet": 0, "lapzero": 1}
+BC = {"dirichlet": 0, "lapzero": 1, "msd": 2}
 DTYPE = {"c64": 0, "c128": 1}
 VKIND = {"none": 0, "harmonic": 1, "array": 2}
 

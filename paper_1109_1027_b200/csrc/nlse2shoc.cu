@@ -539,7 +539,10 @@ static nlse2shoc_status create_impl(nlse2shoc_t *out, int dims, const int64_t N[
   }
   if (!finite_pos(a)) return fail(NLSE2SHOC_EINVAL, "a must be finite and > 0");
   if (!std::isfinite(s)) return fail(NLSE2SHOC_EINVAL, "s must be finite");
-  if (bc != NLSE2SHOC_BC_DIRICHLET && bc != NLSE2SHOC_BC_LAPZERO) return fail(NLSE2SHOC_EINVAL, "bad bc");
+  if (bc != NLSE2SHOC_BC_DIRICHLET && bc != NLSE2SHOC_BC_LAPZERO && bc != NLSE2SHOC_BC_MSD)
+    return fail(NLSE2SHOC_EINVAL, "bad bc");
+  if (bc == NLSE2SHOC_BC_MSD && dims != 1)
+    return fail(NLSE2SHOC_EUNSUPPORTED, "the MSD boundary is implemented for 1D grids only");
   if (dtype != NLSE2SHOC_C64 && dtype != NLSE2SHOC_C128) return fail(NLSE2SHOC_EINVAL, "bad dtype");
   nlse2shoc_potential pv{};
   pv.kind = NLSE2SHOC_V_NONE;

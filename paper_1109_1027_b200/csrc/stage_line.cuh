@@ -9,26 +9,59 @@
 
 namespace nlse {
 
+// MSD boundary (`msdbc_lap`; reading R28): at boundary b with inward
+// neighbour q, lambda_b = [Re(D_q / Psi_q) + (N_q - N_b)/a] Psi_b, D_q = delta^2 Psi at q.
+template <typename R>
+__device__ __forceinline__ cplx<R> msd_lambda(const cplx<R> *__restrict__ Tin, int b, int q, const StageParams<R> &P) {
+  using CT = cplx<R>;
+  const CT cb = Tin[b], cq = Tin[q], cf = Tin[2 * q - b];
+  const CT D = P.ihx2 * ((cb + cf) - R(2) * cq);
+  const R nq = norm2(cq);
+  const R re = fma(D.re, cq.re, D.im * cq.im) / nq;
+  const R Nq = fma(P.s, nq, -potential(P, q, 0, 0)), Nb = fma(P.s, norm2(cb), -potential(P, b, 0, 0));
+  return (re + (Nq - Nb) * P.inv_a) * cb;
+}
+
+template <typename R>
+__device__ __forceinline__ cplx<R> line_lambda(const cplx<R> *__restrict__ Tin, int b, int n, const StageParams<R> &P) {
+  if (P.bc == 2) return msd_lambda(Tin, b, b == 0 ? 1 : n - 2, P);
+  return lambda_b(P, Tin[b], potential(P, b, 0, 0));
+}
+
+// Interior point i of the 1D stage: the 5-point wide form with ghost values at the ends
+// (ghost = h^2 lambda_b + 2 Psi_b - Psi_{b+n}); returns t with F = i t.
+template <typename R>
+__device__ __forceinline__ cplx<R> line_interior(const cplx<R> *__restrict__ Tin, int64_t i, int n,
+                                                const StageParams<R> &P, cplx<R> &c, cplx<R> &L) {
+  using CT = cplx<R>;
+  c = Tin[i];
+  const CT m1 = Tin[i - 1], p1 = Tin[i + 1];
+  CT m2, p2;
+  if (i >= 2) m2 = Tin[i - 2];
+  else m2 = axpy(R(2) * m1 - c, P.hx2, line_lambda(Tin, 0, n, P));
+  if (i <= n - 3) p2 = Tin[i + 2];
+  else p2 = axpy(R(2) * p1 - c, P.hx2, line_lambda(Tin, n - 1, n, P));
+  L = P.cx * (R(16) * (m1 + p1) - (m2 + p2) - R(30) * c);
+  const R N = fma(P.s, norm2(c), -potential(P, int(i), 0, 0));
+  return axpy(N * c, P.a, L);  // a L + N c
+}
+
 // One point of the 1D stage: returns t with F = i t (and L for the Laplacian output).
 template <typename R>
 __device__ __forceinline__ cplx<R> line_point(const cplx<R> *__restrict__ Tin, int64_t i, int n, const StageParams<R> &P,
                                              cplx<R> &c, cplx<R> &L) {
   using CT = cplx<R>;
+  if (i != 0 && i != n - 1) return line_interior(Tin, i, n, P, c, L);
   c = Tin[i];
-  const bool bnd = i == 0 || i == n - 1;
-  const R V = potential(P, int(i), 0, 0);
-  const R N = fma(P.s, norm2(c), -V);
-  if (!bnd) {
-    const CT m1 = Tin[i - 1], p1 = Tin[i + 1];
-    CT m2, p2;
-    if (i >= 2) m2 = Tin[i - 2];
-    else m2 = axpy(R(2) * m1 - c, P.hx2, lambda_b(P, m1, potential(P, 0, 0, 0)));
-    if (i <= n - 3) p2 = Tin[i + 2];
-    else p2 = axpy(R(2) * p1 - c, P.hx2, lambda_b(P, p1, potential(P, n - 1, 0, 0)));
-    L = P.cx * (R(16) * (m1 + p1) - (m2 + p2) - R(30) * c);
-    return axpy(N * c, P.a, L);  // a L + N c
+  L = line_lambda(Tin, int(i), n, P);
+  if (P.bc == 2) {
+    // `msdbc_ut`: Psi_t,b = i Im(Psi_t,q / Psi_q) Psi_b, i.e. t_b = Re(t_q / Psi_q) Psi_b
+    const int q = i == 0 ? 1 : n - 2;
+    CT cq, Lq;
+    const CT tq = line_interior(Tin, q, n, P, cq, Lq);
+    return (fma(tq.re, cq.re, tq.im * cq.im) / norm2(cq)) * c;
   }
-  L = lambda_b(P, c, V);
+  const R N = fma(P.s, norm2(c), -potential(P, int(i), 0, 0));
   return P.bc == 0 ? mk<R>(R(0), R(0)) : N * c;
 }
 

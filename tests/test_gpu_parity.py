@@ -281,3 +281,57 @@ def test_C4_core_box_full_step_count(dtype, variant):
     S.rk4(g, dt, w["steps"])
     ref = oracle.rk4(P, psi.astype(np.complex128), dt, w["steps"])
     assert H.rel_l2(g.cpu().numpy(), ref) <= H.TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype,nsteps", [("c128", 400), ("c64", 400)])
+def test_msd_1d_parity(dtype, nsteps):
+    """MSD boundary (1D) on the paper's co-moving dark soliton (Exp. 1)."""
+    w = configs.EXP_DARK(0.25)
+    psi = H.psi0_host(w, dtype)
+    P = H.oracle_problem(w)
+    S = H.gpu_solver(w, dtype)
+    g = _dev(psi)
+    S.rk4(g, 5e-4, nsteps)
+    ref = oracle.rk4(P, psi.astype(np.complex128), 5e-4, nsteps)
+    assert H.rel_l2(g.cpu().numpy(), ref) <= H.TOL[dtype]
+    L = S.laplacian(_dev(psi)).cpu().numpy()
+    Lo = oracle.laplacian(P, psi.astype(np.complex128))
+    if dtype == "c128":
+        assert H.rel_l2(L, Lo) <= 1e-12
+    else:
+        # fp32 stencil rounding: |dL| <~ 4 u (64/12) |Psi| / h^2 per point (sum of |coefficients|
+        # 64/12 of the 5-point form); the near-constant dark soliton makes L small, so the
+        # relative bound of the other cases does not apply here.
+        u = np.finfo(np.float32).eps / 2
+        h = w["grid"]["h"][0]
+        assert np.linalg.norm(L - Lo) <= 4 * u * (64 / 12) / h**2 * np.linalg.norm(psi)
+
+
+def test_fig1_on_gpu():
+    """The paper's Fig. 1 reproduced by the CUDA library: 2SHOC errors at
+    h = 1/2 ... 1/32 (20000 RK4 steps each, MSD boundary) within 0.5 % of the printed
+    values (domain reading R5), orders within 0.005."""
+    import icgen
+    from oracle import metrics
+    from conftest import read_golden
+
+    gold = {float(r[1]): (float(r[2]), float(r[3])) for r in read_golden("fig1_1d.txt") if r[0] == "2shoc"}
+    E = {}
+    for h in (0.5, 0.25, 0.125, 0.0625, 0.03125):
+        w = configs.EXP_DARK(h)
+        S = H.gpu_solver(w, "c128")
+        g = _dev(H.psi0_host(w, "c128"))
+        per = w["steps"] // 100
+        Er, Ei = [], []
+        for j in range(1, 101):
+            S.rk4(g, 5e-4, per)
+            ic = dict(w["ic"])
+            ic["p"] = list(ic["p"][:4]) + [j * per * 5e-4]
+            er, ei = metrics.rms_err(g.cpu().numpy(), icgen.fill(ic, w["grid"]))
+            Er.append(er)
+            Ei.append(ei)
+        E[h] = (np.mean(Er), np.mean(Ei))
+        assert abs(E[h][0] / gold[h][0] - 1) < 5e-3 and abs(E[h][1] / gold[h][1] - 1) < 5e-3, (h, E[h], gold[h])
+    printed = {0.25: 3.9355, 0.125: 3.9788, 0.0625: 3.9941, 0.03125: 3.9984}
+    for h2, o in printed.items():
+        assert abs(metrics.order(E[2 * h2][0], E[h2][0], 2 * h2, h2) - o) < 5e-3
