@@ -124,9 +124,10 @@ size_t nlse2shoc_workspace_bytes(nlse2shoc_t);
 
 /* 0 = FUSED (default): one kernel per RK4 stage computes the whole 2SHOC Laplacian (both
  *     steps, D never stored), the RHS and the RK4 stage combine.  2D/3D use the
- *     reconstructed-accumulator form: stage 1 stores only T_A = Psi + k/2 K1 and stage 2
+ *     reconstructed-accumulator form: stage 1 stores only T_A = Psi + k/2 K1, stage 2
  *     forms acc = Psi + (T_A - Psi)/3 + k/3 K2 (= Psi + k/6 K1 + k/3 K2 in exact arithmetic),
- *     14 field transfers per point-step.
+ *     stage 3 stores only T_A = Psi + k K3 and stage 4 forms Psi' = acc + (T_A - Psi)/3 +
+ *     k/6 K4: 13 field transfers per point-step.
  * 1 = TWO_KERNEL: the paper's single-storage scheme (`2d2shocs1/2`, `3d2shocs`):
  *     kernel A stores D = sum_d delta_d^2 Psi (D_b = lambda_b), kernel B applies step 2 +
  *     RHS + combine.  One more field of workspace (allocated on first use).
@@ -134,6 +135,14 @@ size_t nlse2shoc_workspace_bytes(nlse2shoc_t);
  *     point-step, the SURVEY §8(a) a6 form).
  * EINVAL for other values.                                                             */
 nlse2shoc_status nlse2shoc_set_variant(nlse2shoc_t, int variant);
+
+/* Spatial scheme (default 2SHOC).  CD = the paper's second-order comparison scheme RK4+CD
+ * (`uttmp`): Lap = sum_d delta_d^2 Psi, same boundary rules (L_b = lambda_b,
+ * F_b per the BC), same kernels with the +-2 weights set to zero.  stability_bound then uses
+ * the CD Gershgorin interval (reading R29).  EUNSUPPORTED with variant 1 (the
+ * two-kernel variant is the paper's 2SHOC storage scheme); EINVAL for other values.     */
+typedef enum { NLSE2SHOC_SCHEME_2SHOC = 0, NLSE2SHOC_SCHEME_CD = 1 } nlse2shoc_scheme;
+nlse2shoc_status nlse2shoc_set_scheme(nlse2shoc_t, int scheme);
 
 /* L = Lap(psi) by 2SHOC; boundary points get L_b = lambda_b.  psi, L: device,
  * field layout, distinct.  Sharded: halo exchange included (collective).             */

@@ -148,6 +148,11 @@ class Solver:
     def set_variant(self, variant: int):
         check(lib().nlse2shoc_set_variant(self._h, int(variant)), "set_variant")
 
+    def set_scheme(self, scheme):
+        """0/"2shoc" (default) or 1/"cd" (the paper's RK4+CD comparison scheme)."""
+        code = {"2shoc": 0, "cd": 1}.get(scheme, scheme)
+        check(lib().nlse2shoc_set_scheme(self._h, int(code)), "set_scheme")
+
     def laplacian(self, psi, out=None, stream=None):
         import torch
 

@@ -78,7 +78,7 @@ struct nlse2shoc_s {
   double h[3] = {1, 1, 1};
   double a = 1, s = 0;
   nlse2shoc_potential V{};
-  int bc = 0, dtype = 0, device = 0, variant = 0;
+  int bc = 0, dtype = 0, device = 0, variant = 0, scheme = 0;
   size_t S = 8;  // bytes per complex
   // slab (streamed axis = dims-1)
   int rank = 0, nranks = 1;
@@ -181,11 +181,27 @@ template <typename R> static void fill_params(nlse2shoc_t H, StageParams<R> &P) 
   P.plane = H->plane;
   // physical spacing of kernel axes: x = axis 0; y = axis 1 (3D); streamed = axis dims-1
   const double hx = H->h[0], hy = H->dims == 3 ? H->h[1] : 1.0, hz = H->dims >= 2 ? H->h[H->dims - 1] : 1.0;
-  P.cx = R(1.0 / (12.0 * hx * hx));
-  P.cy = R(1.0 / (12.0 * hy * hy));
-  P.cz = R(1.0 / (12.0 * hz * hz));
-  P.c30 = R(30.0 * (1.0 / (12.0 * hx * hx) + (H->dims == 3 ? 1.0 / (12.0 * hy * hy) : 0.0) +
-                    (H->dims >= 2 ? 1.0 / (12.0 * hz * hz) : 0.0)));
+  const double hh[3] = {hx * hx, hy * hy, hz * hz};
+  const bool has[3] = {true, H->dims == 3, H->dims >= 2};
+  double w0 = 0.0, w1[3], w2[3];
+  for (int d = 0; d < 3; ++d) {
+    if (H->scheme == NLSE2SHOC_SCHEME_CD) {  // `uttmp`: delta^2 per axis
+      w1[d] = 1.0 / hh[d];
+      w2[d] = 0.0;
+      if (has[d]) w0 += 2.0 / hh[d];
+    } else {  // 5-point wide form of the two-step scheme: (16, -1, -30)/(12 h^2)
+      w1[d] = 16.0 / (12.0 * hh[d]);
+      w2[d] = 1.0 / (12.0 * hh[d]);
+      if (has[d]) w0 += 30.0 / (12.0 * hh[d]);
+    }
+  }
+  P.cx = R(w2[0]);
+  P.cy = R(w2[1]);
+  P.cz = R(w2[2]);
+  P.c1x = R(w1[0]);
+  P.c1y = R(w1[1]);
+  P.c1z = R(w1[2]);
+  P.c30 = R(w0);
   P.ihx2 = R(1.0 / (hx * hx));
   P.ihy2 = R(1.0 / (hy * hy));
   P.ihz2 = R(1.0 / (hz * hz));
@@ -853,9 +869,22 @@ nlse2shoc_status nlse2shoc_set_variant(nlse2shoc_t H, int variant) {
   if (!H) return fail(NLSE2SHOC_EINVAL, "NULL handle");
   if (variant < 0 || variant > 2)
     return fail(NLSE2SHOC_EINVAL, "variant must be 0 (fused), 1 (two-kernel) or 2 (fused, 16-transfer accumulator)");
+  if (variant == 1 && H->scheme != NLSE2SHOC_SCHEME_2SHOC)
+    return fail(NLSE2SHOC_EUNSUPPORTED, "the two-kernel variant is a 2SHOC form");
   for (nlse2shoc_t S : H->slabs) TRY(nlse2shoc_set_variant(S, variant));
   if (variant == 1 && H->slabs.empty()) TRY(ensure_D(H));
   H->variant = variant;
+  return NLSE2SHOC_OK;
+}
+
+nlse2shoc_status nlse2shoc_set_scheme(nlse2shoc_t H, int scheme) {
+  if (!H) return fail(NLSE2SHOC_EINVAL, "NULL handle");
+  if (scheme != NLSE2SHOC_SCHEME_2SHOC && scheme != NLSE2SHOC_SCHEME_CD)
+    return fail(NLSE2SHOC_EINVAL, "scheme must be 0 (2SHOC) or 1 (CD)");
+  if (scheme == NLSE2SHOC_SCHEME_CD && H->variant == 1)
+    return fail(NLSE2SHOC_EUNSUPPORTED, "the two-kernel variant is a 2SHOC form");
+  for (nlse2shoc_t S : H->slabs) TRY(nlse2shoc_set_scheme(S, scheme));
+  H->scheme = scheme;
   return NLSE2SHOC_OK;
 }
 
@@ -907,10 +936,12 @@ nlse2shoc_status nlse2shoc_stability_bound(nlse2shoc_t H, const void *psi, doubl
   // G (Table 2) spanning [-4d/12, 64d/12] (Gershgorin endpoints of -h^2 Lap).  Written for a
   // per-axis sum so that anisotropic h reduces to it (reading R17): with H = sum_d 1/h_d^2 the
   // spectrum of (a Lap + N) lies in [Nmin - (64/12) a H, Nmax + (4/12) a H].
+  // CD (reading R29): -h^2 delta^2 has Gershgorin interval [0, 4] per axis.
   double Hs = 0.0;
   for (int d = 0; d < H->dims; ++d) Hs += 1.0 / (H->h[d] * H->h[d]);
-  const double m1 = std::fabs((64.0 / 12.0) * H->a * Hs - r[0]);
-  const double m2 = std::fabs(r[1] + (4.0 / 12.0) * H->a * Hs);
+  const bool cd = H->scheme == NLSE2SHOC_SCHEME_CD;
+  const double m1 = std::fabs((cd ? 4.0 : 64.0 / 12.0) * H->a * Hs - r[0]);
+  const double m2 = std::fabs(r[1] + (cd ? 0.0 : 4.0 / 12.0) * H->a * Hs);
   *kmax = std::sqrt(8.0) / std::max(m1, m2);
   if (r[2] > 0) return fail(NLSE2SHOC_ENONFINITE, "psi contains non-finite values");
   return NLSE2SHOC_OK;

@@ -41,7 +41,7 @@ __device__ __forceinline__ cplx<R> line_interior(const cplx<R> *__restrict__ Tin
   else m2 = axpy(R(2) * m1 - c, P.hx2, line_lambda(Tin, 0, n, P));
   if (i <= n - 3) p2 = Tin[i + 2];
   else p2 = axpy(R(2) * p1 - c, P.hx2, line_lambda(Tin, n - 1, n, P));
-  L = P.cx * (R(16) * (m1 + p1) - (m2 + p2) - R(30) * c);
+  L = axpy(axpy((-P.c30) * c, P.c1x, m1 + p1), -P.cx, m2 + p2);  // 2SHOC wide form, or CD (cx = 0)
   const R N = fma(P.s, norm2(c), -potential(P, int(i), 0, 0));
   return axpy(N * c, P.a, L);  // a L + N c
 }

@@ -107,13 +107,14 @@ template <typename R> struct StageParams {
   int ntiles;
   int64_t pitch;         // elements per x-row (all buffers)
   int64_t plane;         // elements per plane = pitch * ny
-  R cx, cy, cz;          // 1/(12 h^2) per axis (wide-stencil scale)
-  R c30;                 // 30 (cx + cy + cz): centre weight of the summed wide stencil
+  R cx, cy, cz;          // weight of the +-2 neighbours per axis: 1/(12 h^2) (2SHOC), 0 (CD)
+  R c1x, c1y, c1z;       // weight of the +-1 neighbours: 16/(12 h^2) (2SHOC), 1/h^2 (CD)
+  R c30;                 // centre weight of the summed stencil: 30 sum cx (2SHOC), 2 sum 1/h^2 (CD)
   R ihx2, ihy2, ihz2;    // 1/h^2 per axis (delta^2 in the face rule)
   R hx2, hy2, hz2;       // h^2 per axis (ghost formula)
   R a, s, inv_a;
   R ca, cb;              // stage-combine coefficients (acc, T)
-  int bc;                // 0 Dirichlet, 1 Laplacian-zero
+  int bc;                // 0 Dirichlet, 1 Laplacian-zero, 2 MSD (1D line kernels only)
   int vkind;             // 0 none, 1 harmonic tables, 2 array
   const R *vx, *vy, *vz; // harmonic tables (vz indexed by GLOBAL streamed index)
   const R *varr;         // array potential (local slab, row pitch nx)
@@ -390,7 +391,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
   const int ly0 = rg * RPW;                        // first local row of this thread
   const CT zero = mk<R>(R(0), R(0));
   const R cx = P.cx, cy = P.cy, cz = P.cz, c30 = P.c30, pa_ = P.a, ps_ = P.s, ca = P.ca, cb = P.cb;
-  const R c16x = R(16) * cx, c16y = R(16) * cy, c16z = R(16) * cz;
+  const R c16x = P.c1x, c16y = P.c1y, c16z = P.c1z;
   const int nx = P.nx, ny = P.ny, nz = P.nz, NZ = P.NZ, z0 = P.z0;
   uint32_t tcnt = 0, pcnt = 0;
   auto inc = [](int v, int m) { return v + 1 == m ? 0 : v + 1; };

@@ -48,11 +48,13 @@ def V_array_device(work, dtype):
     return torch.from_numpy(V.astype(np.float32 if dtype == "c64" else np.float64)).cuda()
 
 
-def gpu_solver(work, dtype, variant=0):
+def gpu_solver(work, dtype, variant=0, scheme="2shoc"):
     import paper_1109_1027_b200 as nl
 
     Varr = V_array_device(work, dtype) if work["V"]["kind"] == "array" else None
     S = nl.solver_from_work(work, dtype, V_array=Varr)
+    if scheme != "2shoc":
+        S.set_scheme(scheme)
     if variant:
         S.set_variant(variant)
     S._varr = Varr

@@ -1,0 +1,141 @@
+"""GPU: the CD comparison scheme (`uttmp` P:103-107) at parity with the
+oracle, and the paper's full accuracy tables (Figs. 2-3, f2) reproduced by the CUDA library.
+
+Fig. 2/3 runs use the library in c128 exactly as a user would (Solver.rk4 over 100 snapshot
+intervals, readings R1-R4); the exact solution exp(-r^2/2) e^{-i d t} (`2dexpsol`,
+`3dexpsol`) is formed from icgen's t = 0 amplitude times the phase."""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from icgen import configs
+
+import harness as H
+from conftest import read_golden
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+CASES = [
+    (1, (37,), "dirichlet"), (1, (1001,), "lapzero"),
+    (2, (37, 13), "dirichlet"), (2, (530, 9), "lapzero"),
+    (3, (37, 19, 9), "dirichlet"), (3, (70, 35, 11), "lapzero"),
+]
+
+
+@pytest.mark.parametrize("dims,n,bc", CASES)
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("variant", [0, 2])
+def test_cd_parity(dims, n, bc, dtype, variant):
+    w = configs.SMALL(dims, n, bc, dtype)
+    psi = H.psi0_host(w, dtype)
+    P = H.oracle_problem(w, scheme="cd")
+    S = H.gpu_solver(w, dtype, variant=variant, scheme="cd")
+    L = S.laplacian(_dev(psi)).cpu().numpy()
+    Lo = oracle.laplacian(P, psi.astype(np.complex128))
+    assert H.rel_l2(L, Lo) <= (1e-12 if dtype == "c128" else 1e-5)
+    g = _dev(psi)
+    dt = 0.5 * S.stability_bound(g)
+    S.rk4(g, dt, 20)
+    ref = oracle.rk4(P, psi.astype(np.complex128), dt, 20)
+    assert H.rel_l2(g.cpu().numpy(), ref) <= H.TOL[dtype]
+
+
+def test_cd_msd_parity():
+    w = configs.EXP_DARK(0.25)
+    psi = H.psi0_host(w, "c128")
+    P = oracle.Problem(1, w["grid"]["n"][:1], w["grid"]["h"][:1], w["a"], w["s"], None, "msd", scheme="cd")
+    S = H.gpu_solver(w, "c128", scheme="cd")
+    g = _dev(psi)
+    S.rk4(g, 5e-4, 300)
+    assert H.rel_l2(g.cpu().numpy(), oracle.rk4(P, psi, 5e-4, 300)) <= 1e-12
+
+
+def test_cd_rejects_two_kernel_variant():
+    from paper_1109_1027_b200._lib import NLSE2SHOCError
+
+    w = configs.SMALL(2, (9, 9), "dirichlet")
+    S = H.gpu_solver(w, "c128", scheme="cd")
+    with pytest.raises(NLSE2SHOCError):
+        S.set_variant(1)
+    S2 = H.gpu_solver(w, "c128", variant=1)
+    with pytest.raises(NLSE2SHOCError):
+        S2.set_scheme("cd")
+
+
+@pytest.mark.parametrize("dims,n", [(1, 40), (2, 14)])
+def test_cd_stability_bound_vs_spectrum(dims, n):
+    """k_max rho(a A_cd + diag N) <= sqrt(8) (RK4 stability on the imaginary axis), and the
+    bound is within 15 % of the actual spectral radius (reading R29)."""
+    w = configs.SMALL(dims, (n,) * dims, "dirichlet", h=[0.2] * dims)
+    P = H.oracle_problem(w, scheme="cd")
+    psi = H.psi0_host(w, "c128")
+    S = H.gpu_solver(w, "c128", scheme="cd")
+    kmax = S.stability_bound(_dev(psi))
+    shape = psi.shape
+    I = tuple(slice(1, -1) for _ in range(dims))
+    idx = np.argwhere(np.ones(tuple(m - 2 for m in shape), bool)) + 1
+    A = np.zeros((len(idx), len(idx)))
+    for q, ii in enumerate(idx):
+        e = np.zeros(shape, complex)
+        e[tuple(ii)] = 1.0
+        Pz = oracle.Problem(dims, list(shape[::-1]), w["grid"]["h"][:dims], w["a"], 0.0, None, "dirichlet", "cd")
+        A[:, q] = oracle.laplacian(Pz, e)[I].reshape(-1).real
+    Vp = P.V if P.V is not None else 0.0
+    N = (w["s"] * np.abs(psi) ** 2 - Vp)[I].reshape(-1)
+    rho = np.max(np.abs(np.linalg.eigvals(w["a"] * A + np.diag(N))))
+    assert kmax * rho <= math.sqrt(8) * (1 + 1e-12)
+    assert kmax * rho >= 0.85 * math.sqrt(8)
+
+
+# ----------------------------------------------------------------------------- f2
+def printed_tol(s):
+    mant = s.lower().split("e")[0]
+    exp = int(s.lower().split("e")[1]) if "e" in s.lower() else 0
+    dec = len(mant.split(".")[1]) if "." in mant else 0
+    return 10.0 ** (exp - dec)
+
+
+def run_exp_gpu(dims, h, scheme):
+    import icgen
+
+    w = configs.EXP_GAUSS(dims, h)
+    S = H.gpu_solver(w, "c128", scheme=scheme)
+    amp = _dev(icgen.fill(w["ic"], w["grid"]).real.copy())
+    g = amp.to(torch.complex128).clone()
+    k = w["dt_rule"][1]
+    per = w["steps"] // 100
+    n = amp.numel()
+    Er = torch.zeros((), dtype=torch.float64, device="cuda")
+    Ei = torch.zeros_like(Er)
+    for j in range(1, 101):
+        S.rk4(g, k, per)
+        t = j * per * k
+        e = g - amp * complex(math.cos(dims * t), -math.sin(dims * t))
+        Er += torch.sqrt(torch.sum(e.real ** 2) / n)
+        Ei += torch.sqrt(torch.sum(e.imag ** 2) / n)
+    return float(Er) / 100, float(Ei) / 100
+
+
+FIG_ROWS = [(d, s, h) for d in (2, 3) for s in ("2shoc", "cd") for h in (1.0, 0.5, 0.25, 0.125, 0.0625)]
+
+
+@pytest.mark.parametrize("dims,scheme,h", FIG_ROWS)
+def test_fig2_fig3_on_gpu(dims, scheme, h):
+    """Every row of Fig. 2 and Fig. 3, both schemes, h = 1 ... 1/16,
+    to one unit of the printed digit (the oracle checks the coarse rows, P4/P5)."""
+    er, ei = run_exp_gpu(dims, h, scheme)
+    name = "fig2_2d.txt" if dims == 2 else "fig3_3d.txt"
+    row = [r for r in read_golden(name) if r[0] == scheme and abs(float(r[1]) - h) < 1e-12][0]
+    assert abs(er - float(row[2])) <= printed_tol(row[2]), (er, row)
+    assert abs(ei - float(row[3])) <= printed_tol(row[3]), (ei, row)
