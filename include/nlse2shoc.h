@@ -133,6 +133,11 @@ size_t nlse2shoc_workspace_bytes(nlse2shoc_t);
  *     RHS + combine.  One more field of workspace (allocated on first use).
  * 2 = FUSED_ACC16: as 0 but stage 1 stores acc = Psi + k/6 K1 explicitly (16 transfers per
  *     point-step, the SURVEY §8(a) a6 form).
+ * 3 = TWO_KERNEL_MS: the paper's multi-storage scheme (`2d2shocMs1/2` P:185-200,
+ *     `3d2shocMs1/2` P:262-280, the "2X/3X storage" rows of Tables 4-5): kernel A stores
+ *     D_d = delta_d^2 Psi per axis (face rule of DESIGN.md reading R8 at d-faces), kernel B
+ *     applies L = sum_d 7/6 D_d - (D_d(+e_d) + D_d(-e_d))/12.  dims more fields of workspace.
+ * Variants 1 and 3 are 2SHOC forms: EUNSUPPORTED with the CD scheme.
  * EINVAL for other values.                                                             */
 nlse2shoc_status nlse2shoc_set_variant(nlse2shoc_t, int variant);
 

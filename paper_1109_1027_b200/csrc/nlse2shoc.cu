@@ -79,6 +79,7 @@ struct nlse2shoc_s {
   double a = 1, s = 0;
   nlse2shoc_potential V{};
   int bc = 0, dtype = 0, device = 0, variant = 0, scheme = 0;
+  int D_fields = 0;  // D fields allocated for the two-kernel variants
   size_t S = 8;  // bytes per complex
   // slab (streamed axis = dims-1)
   int rank = 0, nranks = 1;
@@ -330,6 +331,9 @@ static nlse2shoc_status halo_exchange(nlse2shoc_t H, Field &f, cudaStream_t st) 
 #endif
 }
 
+// elements of one D field of the two-kernel variants (local planes [-1, nz])
+static int64_t D_field_elems(nlse2shoc_t H) { return H->plane * (H->dims >= 2 ? H->nz + 2 : 1); }
+
 template <int DIMS, typename R>
 static nlse2shoc_status launch_two(int, int stage, const cplx<R> *in, const cplx<R> *lo, const cplx<R> *hi,
                                    const cplx<R> *psi, const cplx<R> *acc, cplx<R> *D, const StageParams<R> &P,
@@ -349,6 +353,16 @@ static Field &stage_input(nlse2shoc_t H, Field &psi, int s) { return (s == 1 || 
 
 template <int DIMS, typename R, int MODE>
 static nlse2shoc_status launch_mode(nlse2shoc_t H, Field &psi, Field &in, StageParams<R> &P, cudaStream_t st) {
+  if (H->variant == 3) {  // two-kernel, multi-storage (per-axis D_d stored)
+    CUDA_TRY((launch_two_ms_impl<DIMS, R>(MODE, reinterpret_cast<const cplx<R> *>(in.ptr),
+                                          reinterpret_cast<const cplx<R> *>(in.halo_lo),
+                                          reinterpret_cast<const cplx<R> *>(in.halo_hi),
+                                          reinterpret_cast<const cplx<R> *>(psi.ptr),
+                                          reinterpret_cast<const cplx<R> *>(H->acc.ptr),
+                                          reinterpret_cast<cplx<R> *>(H->D.ptr), D_field_elems(H), P, st)));
+    H->launches += 2;
+    return NLSE2SHOC_OK;
+  }
   if (H->variant == 1) {  // two-kernel (stored D)
     TwoParams<R> Q;
     two_params<R>(H->dims, H->h, Q);
@@ -462,7 +476,7 @@ template <typename R> static nlse2shoc_status rk4_resident_1d(nlse2shoc_t H, Fie
 }
 
 static bool resident_ok(nlse2shoc_t H) {
-  return H->dims == 1 && H->slabs.empty() && !H->sharded && H->variant != 1 &&
+  return H->dims == 1 && H->slabs.empty() && !H->sharded && H->variant != 1 && H->variant != 3 &&
          size_t(4) * size_t(H->nx) * H->S <= size_t(200) * 1024 && !getenv("NLSE_NO_RESIDENT");
 }
 
@@ -750,12 +764,21 @@ static nlse2shoc_status check_ptr(const void *p, const char *name) {
   return NLSE2SHOC_OK;
 }
 
-static nlse2shoc_status ensure_D(nlse2shoc_t H) {
-  if (H->D.ptr) return NLSE2SHOC_OK;
-  // D on local planes [-1, nz] (seam planes are recomputed from the Psi halo)
-  const size_t bytes = size_t(H->plane) * size_t(H->dims >= 2 ? H->nz + 2 : 1) * H->S;
-  CUDA_TRY(cudaMalloc(&H->D.ptr, bytes));
-  H->bytes += bytes;
+// D fields of the two-kernel variants on local planes [-1, nz] (seam planes are recomputed
+// from the Psi halo): one (single storage, variant 1) or dims (multi-storage, variant 3).
+
+static nlse2shoc_status ensure_D(nlse2shoc_t H, int nfields) {
+  if (H->D.ptr && H->D_fields >= nfields) return NLSE2SHOC_OK;
+  const size_t bytes = size_t(D_field_elems(H)) * H->S;
+  if (H->D.ptr) {
+    CUDA_TRY(cudaFree(H->D.ptr));
+    H->D.ptr = nullptr;
+    H->bytes -= bytes * size_t(H->D_fields);
+    H->D_fields = 0;
+  }
+  CUDA_TRY(cudaMalloc(&H->D.ptr, bytes * size_t(nfields)));
+  H->bytes += bytes * size_t(nfields);
+  H->D_fields = nfields;
   return NLSE2SHOC_OK;
 }
 
@@ -867,12 +890,13 @@ size_t nlse2shoc_workspace_bytes(nlse2shoc_t H) {
 
 nlse2shoc_status nlse2shoc_set_variant(nlse2shoc_t H, int variant) {
   if (!H) return fail(NLSE2SHOC_EINVAL, "NULL handle");
-  if (variant < 0 || variant > 2)
-    return fail(NLSE2SHOC_EINVAL, "variant must be 0 (fused), 1 (two-kernel) or 2 (fused, 16-transfer accumulator)");
-  if (variant == 1 && H->scheme != NLSE2SHOC_SCHEME_2SHOC)
-    return fail(NLSE2SHOC_EUNSUPPORTED, "the two-kernel variant is a 2SHOC form");
+  if (variant < 0 || variant > 3)
+    return fail(NLSE2SHOC_EINVAL, "variant must be 0 (fused), 1 (two-kernel), 2 (fused, 16-transfer "
+                                  "accumulator) or 3 (two-kernel, multi-storage)");
+  if ((variant == 1 || variant == 3) && H->scheme != NLSE2SHOC_SCHEME_2SHOC)
+    return fail(NLSE2SHOC_EUNSUPPORTED, "the two-kernel variants are 2SHOC forms");
   for (nlse2shoc_t S : H->slabs) TRY(nlse2shoc_set_variant(S, variant));
-  if (variant == 1 && H->slabs.empty()) TRY(ensure_D(H));
+  if ((variant == 1 || variant == 3) && H->slabs.empty()) TRY(ensure_D(H, variant == 3 ? H->dims : 1));
   H->variant = variant;
   return NLSE2SHOC_OK;
 }
@@ -881,8 +905,8 @@ nlse2shoc_status nlse2shoc_set_scheme(nlse2shoc_t H, int scheme) {
   if (!H) return fail(NLSE2SHOC_EINVAL, "NULL handle");
   if (scheme != NLSE2SHOC_SCHEME_2SHOC && scheme != NLSE2SHOC_SCHEME_CD)
     return fail(NLSE2SHOC_EINVAL, "scheme must be 0 (2SHOC) or 1 (CD)");
-  if (scheme == NLSE2SHOC_SCHEME_CD && H->variant == 1)
-    return fail(NLSE2SHOC_EUNSUPPORTED, "the two-kernel variant is a 2SHOC form");
+  if (scheme == NLSE2SHOC_SCHEME_CD && (H->variant == 1 || H->variant == 3))
+    return fail(NLSE2SHOC_EUNSUPPORTED, "the two-kernel variants are 2SHOC forms");
   for (nlse2shoc_t S : H->slabs) TRY(nlse2shoc_set_scheme(S, scheme));
   H->scheme = scheme;
   return NLSE2SHOC_OK;

@@ -75,6 +75,23 @@ __global__ void __launch_bounds__(256) two_d_kernel(PlaneView<R> T, cplx<R> *__r
   D[(int64_t(DIMS >= 2 ? lz + 1 : 0)) * P.plane + o] = d;
 }
 
+// Output of kernel B at local index g: L (MODE 5) or the Psi-space RK4 stage combine.
+template <typename R, int MODE>
+__device__ __forceinline__ void two_store(const StageParams<R> &P, int64_t g, cplx<R> c, cplx<R> L, cplx<R> F,
+                                          const cplx<R> *__restrict__ psi, const cplx<R> *__restrict__ acc) {
+  if (MODE == M_LAP) {
+    P.out_T[g] = L;
+  } else if (MODE == M_S1) {
+    P.out_acc[g] = axpy(c, P.ca, F);
+    P.out_T[g] = axpy(c, P.cb, F);
+  } else if (MODE == M_S2 || MODE == M_S3) {
+    P.out_acc[g] = axpy(acc[g], P.ca, F);
+    P.out_T[g] = axpy(psi[g], P.cb, F);
+  } else {
+    P.out_T[g] = axpy(acc[g], P.cb, F);
+  }
+}
+
 // Kernel B: step 2 + F + stage combine (MODE 1-4) or L (MODE 5) on local planes [0, nz).
 template <int DIMS, typename R, int MODE>
 __global__ void __launch_bounds__(256) two_step2_kernel(PlaneView<R> T, const cplx<R> *__restrict__ D,
@@ -141,18 +158,7 @@ __global__ void __launch_bounds__(256) two_step2_kernel(PlaneView<R> T, const cp
     L = lambda_b(P, c, V);
     F = P.bc == 0 ? mk<R>(R(0), R(0)) : mk<R>(-(N * c.im), N * c.re);
   }
-  const int64_t g = int64_t(lz) * P.plane + o;
-  if (MODE == M_LAP) {
-    P.out_T[g] = L;
-  } else if (MODE == M_S1) {
-    P.out_acc[g] = axpy(c, P.ca, F);
-    P.out_T[g] = axpy(c, P.cb, F);
-  } else if (MODE == M_S2 || MODE == M_S3) {
-    P.out_acc[g] = axpy(acc[g], P.ca, F);
-    P.out_T[g] = axpy(psi[g], P.cb, F);
-  } else {
-    P.out_T[g] = axpy(acc[g], P.cb, F);
-  }
+  two_store<R, MODE>(P, int64_t(lz) * P.plane + o, c, L, F, psi, acc);
 }
 
 template <int DIMS, typename R>
@@ -173,6 +179,108 @@ static cudaError_t launch_two_impl(int stage, const cplx<R> *in, const cplx<R> *
     case 3: two_step2_kernel<DIMS, R, M_S3><<<gb, blk, 0, st>>>(T, D, psi, acc, P, Q); break;
     case 4: two_step2_kernel<DIMS, R, M_S4><<<gb, blk, 0, st>>>(T, D, psi, acc, P, Q); break;
     default: two_step2_kernel<DIMS, R, M_LAP><<<gb, blk, 0, st>>>(T, D, psi, acc, P, Q); break;
+  }
+  return cudaGetLastError();
+}
+
+
+// ---------------------------------------------------------------------------------------
+// Multi-storage variant ("TWO_KERNEL_MS", variant 3): the paper's per-axis form
+// (`2d2shocMs1/2` P:185-200, `3d2shocMs1/2` P:262-280; "2X/3X storage" of Tables 4-5).
+// Kernel A stores D_d = delta_d^2 Psi for every axis d (dims fields); at a d-face point b
+// that is interior along the other axes it stores the face rule (reading R8)
+//     D_d(b) = lambda_b - sum_{e != d} delta_e^2 Psi_b,
+// and lambda_b at edge/corner points (never read).  Kernel B:
+//     L = sum_d 7/6 D_d - (D_d(+e_d) + D_d(-e_d)) / 12,   L_b = lambda_b.
+// D_d for axis d (kernel axes x, y, z) lives at D + d * Dfield.
+template <int DIMS, typename R>
+__global__ void __launch_bounds__(256) two_dms_kernel(PlaneView<R> T, cplx<R> *__restrict__ D, int64_t Dfield,
+                                                      const StageParams<R> P) {
+  const int gx = DIMS == 3 ? blockIdx.x * 32 + (threadIdx.x & 31) : blockIdx.x * 256 + threadIdx.x;
+  const int gy = DIMS == 3 ? blockIdx.y * 8 + (threadIdx.x >> 5) : 0;
+  const int lz = DIMS >= 2 ? int(blockIdx.z) - 1 : 0;
+  if (gx >= P.nx || gy >= P.ny) return;
+  const int gz = P.z0 + lz;
+  if (DIMS >= 2 && (gz < 0 || gz >= P.NZ)) return;
+  const cplx<R> *pl = T(DIMS >= 2 ? lz : 0);
+  const int64_t o = int64_t(gy) * P.pitch + gx;
+  const cplx<R> c = pl[o];
+  // kernel axes present: x always, y in 3D, z (streamed) in 2D/3D
+  const bool fx = gx == 0 || gx == P.nx - 1;
+  const bool fy = DIMS == 3 && (gy == 0 || gy == P.ny - 1);
+  const bool fz = DIMS >= 2 && (gz == 0 || gz == P.NZ - 1);
+  const int nf = int(fx) + int(fy) + int(fz);
+  cplx<R> dx = mk<R>(R(0), R(0)), dy = dx, dz = dx;
+  if (!fx) dx = d2(pl[o - 1], c, pl[o + 1], P.ihx2);
+  if (DIMS == 3 && !fy) dy = d2(pl[o - P.pitch], c, pl[o + P.pitch], P.ihy2);
+  if (DIMS >= 2 && !fz) dz = d2(T(lz - 1)[o], c, T(lz + 1)[o], P.ihz2);
+  cplx<R> lam = mk<R>(R(0), R(0));
+  if (nf) lam = lambda_b(P, c, potential(P, gx, gy, lz));
+  // face rule on a single face; lambda_b on edges/corners (never read)
+  if (fx) dx = nf == 1 ? (lam - dy) - dz : lam;
+  if (fy) dy = nf == 1 ? (lam - dx) - dz : lam;
+  if (fz) dz = nf == 1 ? (lam - dx) - dy : lam;
+  const int64_t g = (int64_t(DIMS >= 2 ? lz + 1 : 0)) * P.plane + o;
+  D[g] = dx;
+  if (DIMS == 3) D[Dfield + g] = dy;
+  if (DIMS >= 2) D[(DIMS - 1) * Dfield + g] = dz;
+}
+
+template <int DIMS, typename R, int MODE>
+__global__ void __launch_bounds__(256) two_step2ms_kernel(PlaneView<R> T, const cplx<R> *__restrict__ D,
+                                                          int64_t Dfield, const cplx<R> *__restrict__ psi,
+                                                          const cplx<R> *__restrict__ acc, const StageParams<R> P) {
+  const int gx = DIMS == 3 ? blockIdx.x * 32 + (threadIdx.x & 31) : blockIdx.x * 256 + threadIdx.x;
+  const int gy = DIMS == 3 ? blockIdx.y * 8 + (threadIdx.x >> 5) : 0;
+  const int lz = blockIdx.z;
+  if (gx >= P.nx || gy >= P.ny) return;
+  const int gz = P.z0 + lz;
+  const int64_t o = int64_t(gy) * P.pitch + gx;
+  const cplx<R> c = T(lz)[o];
+  const bool bnd = gx == 0 || gx == P.nx - 1 || (DIMS == 3 && (gy == 0 || gy == P.ny - 1)) ||
+                   (DIMS >= 2 && (gz == 0 || gz == P.NZ - 1));
+  const R V = potential(P, gx, gy, lz);
+  const R N = fma(P.s, norm2(c), -V);
+  cplx<R> L, F;
+  if (!bnd) {
+    const int64_t dzs = DIMS >= 2 ? P.plane : 0;
+    const cplx<R> *Dx = D + (DIMS >= 2 ? int64_t(lz + 1) * P.plane : 0) + o;
+    const R w0 = R(7.0 / 6.0), w1 = R(1.0 / 12.0);
+    L = w0 * Dx[0] - w1 * (Dx[-1] + Dx[1]);
+    if (DIMS == 3) {
+      const cplx<R> *Dy = Dx + Dfield;
+      L = L + (w0 * Dy[0] - w1 * (Dy[-P.pitch] + Dy[P.pitch]));
+    }
+    if (DIMS >= 2) {
+      const cplx<R> *Dz = Dx + (DIMS - 1) * Dfield;
+      L = L + (w0 * Dz[0] - w1 * (Dz[-dzs] + Dz[dzs]));
+    }
+    F = mk<R>(-fma(P.a, L.im, N * c.im), fma(P.a, L.re, N * c.re));
+  } else {
+    L = lambda_b(P, c, V);
+    F = P.bc == 0 ? mk<R>(R(0), R(0)) : mk<R>(-(N * c.im), N * c.re);
+  }
+  two_store<R, MODE>(P, int64_t(lz) * P.plane + o, c, L, F, psi, acc);
+}
+
+template <int DIMS, typename R>
+static cudaError_t launch_two_ms_impl(int stage, const cplx<R> *in, const cplx<R> *lo, const cplx<R> *hi,
+                                      const cplx<R> *psi, const cplx<R> *acc, cplx<R> *D, int64_t Dfield,
+                                      const StageParams<R> &P, cudaStream_t st) {
+  PlaneView<R> T{in, lo ? lo : in, hi ? hi : in, P.nz, P.plane};
+  dim3 blk(256);
+  const int bx = DIMS == 3 ? (P.nx + 31) / 32 : (P.nx + 255) / 256;
+  dim3 ga(bx, DIMS == 3 ? (P.ny + 7) / 8 : 1, DIMS >= 2 ? P.nz + 2 : 1);
+  two_dms_kernel<DIMS, R><<<ga, blk, 0, st>>>(T, D, Dfield, P);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  dim3 gb(bx, DIMS == 3 ? (P.ny + 7) / 8 : 1, DIMS >= 2 ? P.nz : 1);
+  switch (stage) {
+    case 1: two_step2ms_kernel<DIMS, R, M_S1><<<gb, blk, 0, st>>>(T, D, Dfield, psi, acc, P); break;
+    case 2: two_step2ms_kernel<DIMS, R, M_S2><<<gb, blk, 0, st>>>(T, D, Dfield, psi, acc, P); break;
+    case 3: two_step2ms_kernel<DIMS, R, M_S3><<<gb, blk, 0, st>>>(T, D, Dfield, psi, acc, P); break;
+    case 4: two_step2ms_kernel<DIMS, R, M_S4><<<gb, blk, 0, st>>>(T, D, Dfield, psi, acc, P); break;
+    default: two_step2ms_kernel<DIMS, R, M_LAP><<<gb, blk, 0, st>>>(T, D, Dfield, psi, acc, P); break;
   }
   return cudaGetLastError();
 }

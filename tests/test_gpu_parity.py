@@ -44,10 +44,10 @@ for dims in (1, 2, 3):
                 CASES.append((dims, n, dtype, bc, V))
 
 
-@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("variant", [0, 1, 3])
 @pytest.mark.parametrize("dims,n,dtype,bc,V", CASES)
 def test_laplacian_parity(dims, n, dtype, bc, V, variant):
-    w = _small(dims, n, bc, dtype, V, aniso=(variant == 0 or dims != 2))
+    w = _small(dims, n, bc, dtype, V, aniso=(variant != 1 or dims != 2))
     S = H.gpu_solver(w, dtype, variant)
     psi = H.psi0_host(w, dtype)
     L = S.laplacian(_dev(psi))
@@ -57,7 +57,7 @@ def test_laplacian_parity(dims, n, dtype, bc, V, variant):
     assert H.rel_l2(L.cpu().numpy(), Lo) <= tol
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
 @pytest.mark.parametrize("dims,n,dtype,bc,V", CASES[::2])
 def test_rk4_parity_10_steps(dims, n, dtype, bc, V, variant):
     w = _small(dims, n, bc, dtype, V)

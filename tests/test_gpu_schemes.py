@@ -139,3 +139,17 @@ def test_fig2_fig3_on_gpu(dims, scheme, h):
     row = [r for r in read_golden(name) if r[0] == scheme and abs(float(r[1]) - h) < 1e-12][0]
     assert abs(er - float(row[2])) <= printed_tol(row[2]), (er, row)
     assert abs(ei - float(row[3])) <= printed_tol(row[3]), (ei, row)
+
+
+def test_variant_switch_reallocates_D():
+    """1 -> 3 -> 1 on one handle: the D workspace grows to dims fields and results stay at
+    parity (the multi-storage variant, `3d2shocMs1/2`)."""
+    w = configs.SMALL(3, (21, 17, 9), "dirichlet")
+    psi = H.psi0_host(w, "c128")
+    Lo = oracle.laplacian(H.oracle_problem(w), psi)
+    S = H.gpu_solver(w, "c128", variant=1)
+    b1 = S.workspace_bytes
+    for v in (1, 3, 1):
+        S.set_variant(v)
+        assert H.rel_l2(S.laplacian(_dev(psi)).cpu().numpy(), Lo) <= 1e-12
+    assert S.workspace_bytes > b1
