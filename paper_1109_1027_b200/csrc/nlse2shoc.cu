@@ -273,7 +273,6 @@ static nlse2shoc_status launch_stream(nlse2shoc_t H, Field &in, const CUtensorMa
   if (lead > 0) {
     if (H->prog_cap < P.ntiles) {
       if (H->prog) cudaFree(H->prog);
-  if (H->rbar) cudaFree(H->rbar);
       CUDA_TRY(cudaMalloc(&H->prog, sizeof(uint32_t) * P.ntiles));
       CUDA_TRY(cudaMemsetAsync(H->prog, 0, sizeof(uint32_t) * P.ntiles, st));
       H->prog_cap = P.ntiles;

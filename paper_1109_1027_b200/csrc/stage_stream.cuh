@@ -74,20 +74,20 @@ template <> struct Cfg<3, float> : Rings<68 * (NLSE3F_TY + 4) * 8, 64 * NLSE3F_T
 template <> struct Cfg<3, double> : Rings<36 * (28 + 4) * 16, 32 * 28 * 16> {
   static constexpr int TX = 32, TY = 28, PPX = 1, RPW = 2, NCW = 14, NBOX = 1, NBOXP = 1, W = 36;
 };
-// 2D: the streamed axis is y and a "plane" is one row of TX + halo; 4 x-points per thread so
-// the per-row pipeline overhead is amortised (1040-wide slots split into 128-byte-aligned
-// TMA boxes of 208 eight-byte elements).
-#ifndef NLSE2D_PPX
-#define NLSE2D_PPX 1
+// 2D: the streamed axis is y and a "plane" is one row of TX + halo (slots split into
+// 128-byte-aligned TMA boxes of <= 256 eight-byte elements).  Presets (NLSE2D_PRESET, for
+// sweeps; C3 8192^2 ms/step c128 / c64 on one B200, profiles/r01/README.md):
+//   0 = 512 (c64) / 256 (c128)-wide rows, 8 consumer warps, deep rings   1.79 / 3.34
+//   1 = same tile, half-depth rings (2 CTAs/SM)                          1.78 / 3.31
+//   2 = 1024 / 512-wide rows, 4 / 2 points per thread  (default)         1.49 / 2.67
+//   3 = 1024 / 512-wide rows, 16 consumer warps                          1.47 / 2.69
+//   4, 5 = 2048 / 1024-wide rows (register spills)                       2.16, 1.78 / 3.48, 3.47
+//   6 = preset 2 with a shallower T ring                                 1.50 / 2.67
+// Wider rows amortise the per-row barrier round trip over more bytes.
+#ifndef NLSE2D_PRESET
+#define NLSE2D_PRESET 2
 #endif
-#if NLSE2D_PPX == 4
-template <> struct Cfg<2, float> : Rings<1040 * 8, 1024 * 8> {
-  static constexpr int TX = 1024, TY = 1, PPX = 4, RPW = 1, NCW = 8, NBOX = 5, NBOXP = 4, W = 1040;
-};
-template <> struct Cfg<2, double> : Rings<1040 * 16, 1024 * 16> {
-  static constexpr int TX = 1024, TY = 1, PPX = 4, RPW = 1, NCW = 8, NBOX = 10, NBOXP = 8, W = 1040;
-};
-#else
+#if NLSE2D_PRESET == 0
 template <> struct Cfg<2, float> {
   static constexpr int TX = 512, TY = 1, PPX = 2, RPW = 1, NCW = 8, NBOX = 3, NBOXP = 2, W = 528;
   static constexpr int RT0 = 40, RT1 = 24, RP1 = 20, RT2 = 20, RP2 = 12;
@@ -95,6 +95,60 @@ template <> struct Cfg<2, float> {
 template <> struct Cfg<2, double> {
   static constexpr int TX = 256, TY = 1, PPX = 1, RPW = 1, NCW = 8, NBOX = 3, NBOXP = 2, W = 264;
   static constexpr int RT0 = 40, RT1 = 24, RP1 = 20, RT2 = 20, RP2 = 12;
+};
+#elif NLSE2D_PRESET == 1
+template <> struct Cfg<2, float> {
+  static constexpr int TX = 512, TY = 1, PPX = 2, RPW = 1, NCW = 8, NBOX = 3, NBOXP = 2, W = 528;
+  static constexpr int RT0 = 20, RT1 = 12, RP1 = 10, RT2 = 10, RP2 = 6;
+};
+template <> struct Cfg<2, double> {
+  static constexpr int TX = 256, TY = 1, PPX = 1, RPW = 1, NCW = 8, NBOX = 3, NBOXP = 2, W = 264;
+  static constexpr int RT0 = 20, RT1 = 12, RP1 = 10, RT2 = 10, RP2 = 6;
+};
+#elif NLSE2D_PRESET == 2
+template <> struct Cfg<2, float> {
+  static constexpr int TX = 1024, TY = 1, PPX = 4, RPW = 1, NCW = 8, NBOX = 5, NBOXP = 4, W = 1040;
+  static constexpr int RT0 = 24, RT1 = 12, RP1 = 12, RT2 = 10, RP2 = 7;
+};
+template <> struct Cfg<2, double> {
+  static constexpr int TX = 512, TY = 1, PPX = 2, RPW = 1, NCW = 8, NBOX = 5, NBOXP = 4, W = 520;
+  static constexpr int RT0 = 24, RT1 = 12, RP1 = 12, RT2 = 10, RP2 = 7;
+};
+#elif NLSE2D_PRESET == 4
+template <> struct Cfg<2, float> {
+  static constexpr int TX = 2048, TY = 1, PPX = 8, RPW = 1, NCW = 8, NBOX = 10, NBOXP = 8, W = 2080;
+  static constexpr int RT0 = 12, RT1 = 6, RP1 = 6, RT2 = 6, RP2 = 3;
+};
+template <> struct Cfg<2, double> {
+  static constexpr int TX = 1024, TY = 1, PPX = 4, RPW = 1, NCW = 8, NBOX = 10, NBOXP = 8, W = 1040;
+  static constexpr int RT0 = 12, RT1 = 6, RP1 = 6, RT2 = 6, RP2 = 3;
+};
+#elif NLSE2D_PRESET == 5
+template <> struct Cfg<2, float> {
+  static constexpr int TX = 2048, TY = 1, PPX = 4, RPW = 1, NCW = 16, NBOX = 10, NBOXP = 8, W = 2080;
+  static constexpr int RT0 = 12, RT1 = 6, RP1 = 6, RT2 = 6, RP2 = 3;
+};
+template <> struct Cfg<2, double> {
+  static constexpr int TX = 1024, TY = 1, PPX = 2, RPW = 1, NCW = 16, NBOX = 10, NBOXP = 8, W = 1040;
+  static constexpr int RT0 = 12, RT1 = 6, RP1 = 6, RT2 = 6, RP2 = 3;
+};
+#elif NLSE2D_PRESET == 6
+template <> struct Cfg<2, float> {
+  static constexpr int TX = 1024, TY = 1, PPX = 4, RPW = 1, NCW = 8, NBOX = 5, NBOXP = 4, W = 1040;
+  static constexpr int RT0 = 24, RT1 = 14, RP1 = 10, RT2 = 12, RP2 = 6;
+};
+template <> struct Cfg<2, double> {
+  static constexpr int TX = 512, TY = 1, PPX = 2, RPW = 1, NCW = 8, NBOX = 5, NBOXP = 4, W = 520;
+  static constexpr int RT0 = 24, RT1 = 14, RP1 = 10, RT2 = 12, RP2 = 6;
+};
+#else
+template <> struct Cfg<2, float> {
+  static constexpr int TX = 1024, TY = 1, PPX = 2, RPW = 1, NCW = 16, NBOX = 5, NBOXP = 4, W = 1040;
+  static constexpr int RT0 = 24, RT1 = 12, RP1 = 12, RT2 = 10, RP2 = 7;
+};
+template <> struct Cfg<2, double> {
+  static constexpr int TX = 512, TY = 1, PPX = 1, RPW = 1, NCW = 16, NBOX = 5, NBOXP = 4, W = 520;
+  static constexpr int RT0 = 24, RT1 = 12, RP1 = 12, RT2 = 10, RP2 = 7;
 };
 #endif
 
