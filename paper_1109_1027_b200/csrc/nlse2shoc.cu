@@ -17,6 +17,7 @@
 #include "stage_line.cuh"
 #include "stage_stream.cuh"
 #include "two_kernel.cuh"
+#include "stage_pair.cuh"
 
 #ifdef NLSE_WITH_NCCL
 #include <nccl.h>
@@ -70,6 +71,7 @@ struct Field {  // one pitched field of the local slab (+ its two halo buffers w
   void *halo_lo = nullptr, *halo_hi = nullptr;
   CUtensorMap tm{}, tm_lo{}, tm_hi{};  // stencil-input boxes (tile + halo) over the slab / halos
   CUtensorMap tm_pt{};                 // pointwise tile boxes (Psi^n, acc reads)
+  CUtensorMap tm_in4{}, tm_ex{}, tm_ppt{};  // stage-pair kernel: halo-4 input, halo-2 Psi, acc tile
 };
 
 struct nlse2shoc_s {
@@ -164,6 +166,25 @@ template <int DIMS, typename R> struct Maps {
                         H->plane * S, LY::BWP, C::TY);
     return encode_map(tm, base, 2, uint64_t(H->nx) * LY::EPC, uint64_t(H->nz), 1, H->pitch * S, H->plane * S * H->nz,
                       LY::BWP, 1);
+  }
+};
+
+// tensor maps of the stage-pair kernel (stage_pair.cuh geometry)
+template <int DIMS, typename R> struct PMaps {
+  using LY = PLayout<DIMS, R>;
+  using C = PCfg<DIMS, R>;
+  static nlse2shoc_status enc(nlse2shoc_t H, CUtensorMap *tm, void *base, uint32_t bw, uint32_t rows) {
+    const uint64_t S = sizeof(cplx<R>);
+    if (DIMS == 3)
+      return encode_map(tm, base, 3, uint64_t(H->nx) * LY::EPC, uint64_t(H->ny), uint64_t(H->nz), H->pitch * S,
+                        H->plane * S, bw, rows, tma_promo());
+    return encode_map(tm, base, 2, uint64_t(H->nx) * LY::EPC, uint64_t(H->nz), 1, H->pitch * S, H->plane * S * H->nz,
+                      bw, 1, tma_promo());
+  }
+  static nlse2shoc_status all(nlse2shoc_t H, Field &f) {
+    TRY(enc(H, &f.tm_in4, f.ptr, LY::BW_IN, LY::IROWS));
+    TRY(enc(H, &f.tm_ex, f.ptr, LY::BW_EX, LY::EROWS));
+    return enc(H, &f.tm_ppt, f.ptr, LY::BWP, C::TY);
   }
 };
 
@@ -290,6 +311,77 @@ static nlse2shoc_status launch_stream(nlse2shoc_t H, Field &in, const CUtensorMa
                                                                    tm_acc ? *tm_acc : in.tm, P);
   CUDA_TRY(cudaGetLastError());
   ++H->launches;
+  return NLSE2SHOC_OK;
+}
+
+// Stage-pair (temporal blocking) launch, variant 4: one persistent grid per pair.
+template <int DIMS, typename R, int PAIR>
+static nlse2shoc_status launch_pair(nlse2shoc_t H, const CUtensorMap &tin, const CUtensorMap &tps,
+                                    const CUtensorMap &tacc, StageParams<R> P, cudaStream_t st) {
+  using C = PCfg<DIMS, R>;
+  using LY = PLayout<DIMS, R>;
+  const size_t smem = LY::template smem_bytes<PAIR>();
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(pair_stream_kernel<DIMS, R, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(smem)));
+    attr = true;
+  }
+  int occ = 1;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pair_stream_kernel<DIMS, R, PAIR>, LY::NTHREADS, smem));
+  occ = std::max(occ, 1);
+  const int G0 = H->num_sms * occ;
+  P.ncx = int((H->nx + C::TX - 1) / C::TX);
+  P.ncy = DIMS == 3 ? int((H->ny + C::TY - 1) / C::TY) : 1;
+  const int ncol = P.ncx * P.ncy;
+  // z-chunks: minimise rounds * (chunk length + priming cost of 4 extra phase-A planes)
+  int best = 1;
+  double bestc = 1e300;
+  for (int nc = 1; nc <= 256 && nc <= H->nz; ++nc) {
+    const double rounds = std::ceil(double(ncol) * nc / G0);
+    const double c = rounds * (std::ceil(double(H->nz) / nc) + 4.0);
+    if (c < bestc - 1e-9) { bestc = c; best = nc; }
+  }
+  static const int force_chunks = getenv("NLSE_NCHUNK") ? atoi(getenv("NLSE_NCHUNK")) : 0;
+  if (force_chunks > 0) best = std::min<int>(force_chunks, int(H->nz));
+  P.nchunk = best;
+  P.ntiles = ncol * best;
+  const int G = std::min(G0, P.ntiles);
+  pair_stream_kernel<DIMS, R, PAIR><<<G, LY::NTHREADS, smem, st>>>(tin, tps, tacc, P);
+  CUDA_TRY(cudaGetLastError());
+  ++H->launches;
+  return NLSE2SHOC_OK;
+}
+
+// One RK4 step of the stage-pair form: X = Psi^n (read), Y = Psi^{n+1} (written), X != Y.
+template <int DIMS, typename R>
+static nlse2shoc_status pair_step(nlse2shoc_t H, Field &X, Field &Y, double dt, cudaStream_t st) {
+  StageParams<R> P;
+  fill_params<R>(H, P);
+  P.cA = R(dt / 2.0);
+  P.ca = R(dt / 3.0);
+  P.cb = R(dt / 2.0);
+  P.out_T = reinterpret_cast<cplx<R> *>(H->TB.ptr);
+  P.out_acc = reinterpret_cast<cplx<R> *>(H->acc.ptr);
+  TRY((launch_pair<DIMS, R, PAIR_A>(H, X.tm_in4, X.tm_in4, X.tm_in4, P, st)));
+  P.cA = R(dt);
+  P.ca = R(0);
+  P.cb = R(dt / 6.0);
+  P.out_T = reinterpret_cast<cplx<R> *>(Y.ptr);
+  P.out_acc = nullptr;
+  return launch_pair<DIMS, R, PAIR_B>(H, H->TB.tm_in4, X.tm_ex, H->acc.tm_ppt, P, st);
+}
+
+static nlse2shoc_status rk4_pairs(nlse2shoc_t H, Field &psi, double dt, int64_t nsteps, cudaStream_t st) {
+  Field *X = &psi, *Y = &H->TA;
+  const bool f32 = H->dtype == NLSE2SHOC_C64;
+  for (int64_t n = 0; n < nsteps; ++n) {
+    if (H->dims == 3) TRY(f32 ? (pair_step<3, float>(H, *X, *Y, dt, st)) : (pair_step<3, double>(H, *X, *Y, dt, st)));
+    else TRY(f32 ? (pair_step<2, float>(H, *X, *Y, dt, st)) : (pair_step<2, double>(H, *X, *Y, dt, st)));
+    std::swap(X, Y);
+  }
+  if (X != &psi)
+    CUDA_TRY(cudaMemcpyAsync(psi.ptr, X->ptr, size_t(H->local_elems) * H->S, cudaMemcpyDeviceToDevice, st));
   return NLSE2SHOC_OK;
 }
 
@@ -480,6 +572,7 @@ static bool resident_ok(nlse2shoc_t H) {
 }
 
 static nlse2shoc_status run_rk4(View &v, double dt, int64_t nsteps, cudaStream_t st) {
+  if (v.hs.size() == 1 && v.hs[0]->variant == 4) return rk4_pairs(v.hs[0], v.psis[0], dt, nsteps, st);
   if (v.hs.size() == 1 && resident_ok(v.hs[0])) {
     nlse2shoc_t H = v.hs[0];
     return H->dtype == NLSE2SHOC_C64 ? rk4_resident_1d<float>(H, v.psis[0], dt, nsteps, st)
@@ -510,6 +603,10 @@ static nlse2shoc_status alloc_field(nlse2shoc_t H, Field &f, bool halos) {
 }
 
 template <typename R> static nlse2shoc_status encode_field_maps(nlse2shoc_t H, Field &f) {
+  if (H->dims >= 2) {
+    if (H->dims == 3) TRY((PMaps<3, R>::all(H, f)));
+    else TRY((PMaps<2, R>::all(H, f)));
+  }
   if (H->dims == 3) {
     TRY((Maps<3, R>::point(H, &f.tm_pt, f.ptr)));
     TRY((Maps<3, R>::stencil(H, &f.tm, f.ptr, H->nz)));
@@ -889,9 +986,11 @@ size_t nlse2shoc_workspace_bytes(nlse2shoc_t H) {
 
 nlse2shoc_status nlse2shoc_set_variant(nlse2shoc_t H, int variant) {
   if (!H) return fail(NLSE2SHOC_EINVAL, "NULL handle");
-  if (variant < 0 || variant > 3)
+  if (variant < 0 || variant > 4)
     return fail(NLSE2SHOC_EINVAL, "variant must be 0 (fused), 1 (two-kernel), 2 (fused, 16-transfer "
-                                  "accumulator) or 3 (two-kernel, multi-storage)");
+                                  "accumulator), 3 (two-kernel, multi-storage) or 4 (stage pairs)");
+  if (variant == 4 && (H->dims < 2 || !H->slabs.empty() || H->sharded))
+    return fail(NLSE2SHOC_EUNSUPPORTED, "the stage-pair variant needs a single-slab 2D/3D handle");
   if ((variant == 1 || variant == 3) && H->scheme != NLSE2SHOC_SCHEME_2SHOC)
     return fail(NLSE2SHOC_EUNSUPPORTED, "the two-kernel variants are 2SHOC forms");
   for (nlse2shoc_t S : H->slabs) TRY(nlse2shoc_set_variant(S, variant));

@@ -168,6 +168,7 @@ template <typename R> struct StageParams {
   R hx2, hy2, hz2;       // h^2 per axis (ghost formula)
   R a, s, inv_a;
   R ca, cb;              // stage-combine coefficients (acc, T)
+  R cA;                  // phase-A coefficient of the stage-pair kernel (stage_pair.cuh)
   int bc;                // 0 Dirichlet, 1 Laplacian-zero, 2 MSD (1D line kernels only)
   int vkind;             // 0 none, 1 harmonic tables, 2 array
   const R *vx, *vy, *vz; // harmonic tables (vz indexed by GLOBAL streamed index)

@@ -14,6 +14,9 @@ g = w["grid"]
 dims = g["dims"]
 shape = tuple(reversed(g["n"][:dims]))
 S = nl.solver_from_work(w, dtype)
+variant = int(os.environ.get("NLSE_VARIANT", "0"))
+if variant:
+    S.set_variant(variant)
 torch.manual_seed(0)
 tdt = torch.complex64 if dtype == "c64" else torch.complex128
 psi = torch.randn(shape, dtype=tdt, device="cuda") * 0.01 + 1.0
@@ -28,6 +31,6 @@ for rep in range(3):
 ms = min(res)
 n = 1
 for v in shape: n *= v
-print(json.dumps({"lib": os.path.basename(os.environ.get("NLSE_LIB", "default")), "config": name, "dtype": dtype,
+print(json.dumps({"lib": os.path.basename(os.environ.get("NLSE_LIB", "default")), "config": name, "dtype": dtype, "variant": variant,
                   "ms_per_step": round(ms, 4), "pt_steps_s": n / ms * 1e3,
                   "finite": bool(torch.isfinite(torch.view_as_real(psi)).all())}))
