@@ -31,8 +31,11 @@ enum PairKind { PAIR_A = 0, PAIR_B = 1 };
 // W_IN: input slot row (x0-4 ...), W_EX: mid / Psi-ext slot row (x0-2 ...); rings: RI input
 // planes (5 pinned + prefetch), 5 mid planes, RPS Psi-ext planes and RA acc tiles (pair B).
 template <int DIMS, typename R> struct PCfg;
+#ifndef NLSE_PAIR3F_RPW
+#define NLSE_PAIR3F_RPW 2
+#endif
 template <> struct PCfg<3, float> {
-  static constexpr int TX = 64, TY = 16, PPX = 2, RPW = 2, NCW = 8;
+  static constexpr int TX = 64, TY = 16, PPX = 2, RPW = NLSE_PAIR3F_RPW, NCW = 16 / NLSE_PAIR3F_RPW;
   static constexpr int W_IN = 72, NBOX_IN = 1, W_EX = 68, NBOX_EX = 1, NBOXP = 1;
   static constexpr int RI_A = 9, RI_B = 7, RPS = 4, RA = 2;
 };
@@ -265,6 +268,34 @@ __global__ void __launch_bounds__(PLayout<DIMS, R>::NTHREADS, 1)
 #pragma unroll
     for (int r = 0; r < RPW; ++r) vyr[r] = (P.vkind == 1 && P.vy && y0 + ly0 + r < ny) ? P.vy[y0 + ly0 + r] : R(0);
 
+    // phase-A tasks of this thread (tile-constant): input-slot run offset, ext offset and the
+    // x/y part of a separable harmonic V
+    constexpr int NTA = (LY::NTASK_A + NT - 1) / NT;
+    int a_in[NTA], a_ex[NTA];
+    R a_v[NTA][PPX];
+#pragma unroll
+    for (int i = 0; i < NTA; ++i) {
+      const int task = min(ct + i * NT, LY::NTASK_A - 1);
+      const int ex = (task % (LY::EXW / PPX)) * PPX, ey = task / (LY::EXW / PPX);
+      a_in[i] = (ey + HI - HE) * WI + ex;
+      a_ex[i] = ey * WE + ex;
+      const int gy = y0 - HE + ey;
+#pragma unroll
+      for (int q = 0; q < PPX; ++q) {
+        const int gx = x0 - 2 + ex + q;
+        R v = R(0);
+        if (P.vkind == 1 && gx >= 0 && gx < nx && gy >= 0 && gy < ny) {
+          v = P.vx[gx];
+          if (DIMS == 3 && P.vy) v = v + P.vy[gy];
+        }
+        a_v[i][q] = v;
+      }
+    }
+    // lean planes: no boundary point, no ghost, no array potential in the region a phase covers
+    const bool leanA = P.vkind != 2 && x0 - 2 >= 1 && x0 + TX + 2 <= nx - 1 &&
+                       (DIMS == 2 || (y0 - 2 >= 1 && y0 + TY + 2 <= ny - 1));
+    const bool leanB = P.vkind != 2 && x0 >= 1 && x0 + TX <= nx - 1 && (DIMS == 2 || (y0 >= 1 && y0 + TY <= ny - 1));
+
     CT qm2[RPW][PPX], qm1[RPW][PPX], qp1[RPW][PPX];
     cplx<R> *outT = P.out_T + int64_t(kb) * P.plane + int64_t(y0 + ly0) * P.pitch + (x0 + lx0);
     cplx<R> *outA = B ? nullptr : P.out_acc + (outT - P.out_T);
@@ -336,7 +367,51 @@ __global__ void __launch_bounds__(PLayout<DIMS, R>::NTHREADS, 1)
           named_bar_sync(1, NT);
         }
       }
-      if (jin) {
+      if (jin && leanA && gzj >= 2 && gzj <= NZ - 3) {
+        const CT *s0 = islot(j), *sm1 = islot(j - 1), *sm2 = islot(j - 2), *sp1 = islot(j + 1), *sp2 = islot(j + 2);
+        const CT *ps = B ? sslot(j) : nullptr;
+        CT *md = mslot(j);
+        const R vzj = (P.vkind == 1 && P.vz) ? P.vz[z0 + j] : R(0);
+#pragma unroll
+        for (int i = 0; i < NTA; ++i) {
+          // threads without an i-th task redo the last task (same value to the same address)
+          const int o = a_in[i];
+          CT run[PPX + 4];
+          lds_run<R, PPX + 4>(s0 + o, run);
+          CT zm2[PPX], zm1[PPX], zp1[PPX], zp2[PPX];
+          lds_run<R, PPX>(sm2 + o + 2, zm2);
+          lds_run<R, PPX>(sm1 + o + 2, zm1);
+          lds_run<R, PPX>(sp1 + o + 2, zp1);
+          lds_run<R, PPX>(sp2 + o + 2, zp2);
+          CT ym2[PPX], ym1[PPX], yp1[PPX], yp2[PPX];
+          if (DIMS == 3) {
+            lds_run<R, PPX>(s0 + o + 2 - 2 * WI, ym2);
+            lds_run<R, PPX>(s0 + o + 2 - WI, ym1);
+            lds_run<R, PPX>(s0 + o + 2 + WI, yp1);
+            lds_run<R, PPX>(s0 + o + 2 + 2 * WI, yp2);
+          }
+          CT psv[PPX];
+          if (B) lds_run<R, PPX>(ps + a_ex[i], psv);
+          CT out[PPX];
+#pragma unroll
+          for (int q = 0; q < PPX; ++q) {
+            const CT c = run[q + 2];
+            CT L = (-c30) * c;
+            L = axpy(L, c16x, run[q + 1] + run[q + 3]);
+            L = axpy(L, -cx, run[q] + run[q + 4]);
+            L = axpy(L, c16z, zm1[q] + zp1[q]);
+            L = axpy(L, -cz, zm2[q] + zp2[q]);
+            if (DIMS == 3) {
+              L = axpy(L, c16y, ym1[q] + yp1[q]);
+              L = axpy(L, -cy, ym2[q] + yp2[q]);
+            }
+            const R N = fma(ps_, norm2(c), -(a_v[i][q] + vzj));
+            const CT tF = axpy(N * c, pa_, L);
+            out[q] = B ? iaxpy(psv[q], cA, tF) : iaxpy(c, cA, tF);
+          }
+          sts_run<R, PPX>(md + a_ex[i], out);
+        }
+      } else if (jin) {
         const CT *s0 = islot(j), *sm1 = islot(j - 1), *sm2 = islot(j - 2), *sp1 = islot(j + 1), *sp2 = islot(j + 2);
         const CT *ps = B ? sslot(j) : nullptr;
         CT *md = mslot(j);
@@ -438,6 +513,8 @@ __global__ void __launch_bounds__(PLayout<DIMS, R>::NTHREADS, 1)
         }
         const R vzk = (P.vkind == 1 && P.vz) ? P.vz[z0 + k] : R(0);
         const CT *m0 = &atm(mslot(k), lx0, ly0) - 2, *mp2 = &atm(mslot(k + 2), lx0, ly0);
+        auto bloop = [&](auto lean_c) {
+          constexpr bool LEAN = decltype(lean_c)::value;
 #pragma unroll
         for (int r = 0; r < RPW; ++r) {
           const int gy = y0 + ly0 + r;
@@ -445,7 +522,7 @@ __global__ void __launch_bounds__(PLayout<DIMS, R>::NTHREADS, 1)
           lds_run<R, PPX + 4>(m0 + r * WE, run);
           CT zp2[PPX];
           lds_run<R, PPX>(mp2 + r * WE, zp2);
-          if (zg_lo || zg_hi) {
+          if (!LEAN && (zg_lo || zg_hi)) {
             const CT *sbp = &atm(mslot(zg_lo ? k - 1 : k + 1), lx0, ly0 + r);
 #pragma unroll
             for (int q = 0; q < PPX; ++q) {
@@ -490,12 +567,12 @@ __global__ void __launch_bounds__(PLayout<DIMS, R>::NTHREADS, 1)
               L = axpy(L, c16y, ym1[q] + yp1[q]);
               L = axpy(L, -cy, ym2[q] + yp2[q]);
             }
-            valid[q] = gx < nx && gy < ny;
+            valid[q] = LEAN || (gx < nx && gy < ny);
             R V;
-            if (P.vkind == 2) V = valid[q] ? potential(P, gx, gy, k) : R(0);
+            if (!LEAN && P.vkind == 2) V = valid[q] ? potential(P, gx, gy, k) : R(0);
             else V = (vxr[q] + vyr[r]) + vzk;
             const R N = fma(ps_, norm2(c), -V);
-            const bool bnd = gx == 0 || gx == nx - 1 || (DIMS == 3 && (gy == 0 || gy == ny - 1)) || !zint;
+            const bool bnd = !LEAN && (gx == 0 || gx == nx - 1 || (DIMS == 3 && (gy == 0 || gy == ny - 1)) || !zint);
             const CT tF = bnd ? (P.bc == 0 ? zero : N * c) : axpy(N * c, pa_, L);
             if (B) {
               oT[q] = iaxpy(axpy(acv[q], R(1.0 / 3.0), c - psv[q]), cb, tF);
@@ -531,6 +608,9 @@ __global__ void __launch_bounds__(PLayout<DIMS, R>::NTHREADS, 1)
             qp1[r][q] = zp2[q];
           }
         }
+        };
+        if (leanB && gz >= 2 && gz <= NZ - 3) bloop(std::true_type{});
+        else bloop(std::false_type{});
         outT += P.plane;
         if (!B) outA += P.plane;
         if (B) {

@@ -566,6 +566,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
 
       // ---- stencil + RHS + stage combine for this thread's points of plane k
       const CT *s0 = ring + size_t(sk) * LY::SLOT + toff, *sp2 = ring + size_t(sk2) * LY::SLOT + toff;
+      CT ym2[PPX], ym1[PPX], yp1[PPX], yp2[PPX], cprev[PPX];  // y window, rolled down the rows
 #pragma unroll
       for (int r = 0; r < RPW; ++r) {
         const int gy = y0 + ly0 + r;
@@ -591,12 +592,22 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
             else zp2[q] = g;
           }
         }
-        CT ym2[PPX], ym1[PPX], yp1[PPX], yp2[PPX];
         if (DIMS == 3) {
-          lds_run<R, PPX>(s0 + (r - 2) * W + 2, ym2);
-          lds_run<R, PPX>(s0 + (r - 1) * W + 2, ym1);
-          lds_run<R, PPX>(s0 + (r + 1) * W + 2, yp1);
+          if (r == 0) {
+            lds_run<R, PPX>(s0 + (r - 2) * W + 2, ym2);
+            lds_run<R, PPX>(s0 + (r - 1) * W + 2, ym1);
+            lds_run<R, PPX>(s0 + (r + 1) * W + 2, yp1);
+          } else {
+#pragma unroll
+            for (int q = 0; q < PPX; ++q) {
+              ym2[q] = ym1[q];
+              ym1[q] = cprev[q];
+              yp1[q] = yp2[q];
+            }
+          }
           lds_run<R, PPX>(s0 + (r + 2) * W + 2, yp2);
+#pragma unroll
+          for (int q = 0; q < PPX; ++q) cprev[q] = run[q + 2];
         }
         CT psv[PPX], acv[PPX];
         const int poff = (ly0 + r) * TX + lx0;
@@ -716,18 +727,29 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
         pa = pring + size_t(sp) * NPA * LY::PTILE + ly0 * TX + lx0;
       }
       const CT *s0 = ringT + size_t(sk) * LY::SLOT, *sp2 = ringT + size_t(sk2) * LY::SLOT;
+      CT ym2[PPX], ym1[PPX], yp1[PPX], yp2[PPX], cprev[PPX];  // y window, rolled down the rows
 #pragma unroll
       for (int r = 0; r < RPW; ++r) {
         CT run[PPX + 4];
         lds_run<R, PPX + 4>(s0 + r * W, run);
         CT zp2[PPX];
         lds_run<R, PPX>(sp2 + r * W + 2, zp2);
-        CT ym2[PPX], ym1[PPX], yp1[PPX], yp2[PPX];
         if (DIMS == 3) {
-          lds_run<R, PPX>(s0 + (r - 2) * W + 2, ym2);
-          lds_run<R, PPX>(s0 + (r - 1) * W + 2, ym1);
-          lds_run<R, PPX>(s0 + (r + 1) * W + 2, yp1);
+          if (r == 0) {
+            lds_run<R, PPX>(s0 + (r - 2) * W + 2, ym2);
+            lds_run<R, PPX>(s0 + (r - 1) * W + 2, ym1);
+            lds_run<R, PPX>(s0 + (r + 1) * W + 2, yp1);
+          } else {
+#pragma unroll
+            for (int q = 0; q < PPX; ++q) {
+              ym2[q] = ym1[q];
+              ym1[q] = cprev[q];
+              yp1[q] = yp2[q];
+            }
+          }
           lds_run<R, PPX>(s0 + (r + 2) * W + 2, yp2);
+#pragma unroll
+          for (int q = 0; q < PPX; ++q) cprev[q] = run[q + 2];
         }
         CT psv[PPX], acv[PPX];
         if (LY::template needs_psi<MODE>()) lds_run<R, PPX>(pa + r * TX, psv);
