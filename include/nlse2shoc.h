@@ -137,6 +137,12 @@ size_t nlse2shoc_workspace_bytes(nlse2shoc_t);
  *     `3d2shocMs1/2` P:262-280, the "2X/3X storage" rows of Tables 4-5): kernel A stores
  *     D_d = delta_d^2 Psi per axis (face rule of DESIGN.md reading R8 at d-faces), kernel B
  *     applies L = sum_d 7/6 D_d - (D_d(+e_d) + D_d(-e_d))/12.  dims more fields of workspace.
+ * 4 = STAGE_PAIRS (temporal blocking): one launch runs stages 1+2 and one
+ *     runs stages 3+4 over each tile, the first stage of a pair evaluated on the tile grown by
+ *     the stencil radius and kept in shared memory: 7 field transfers per point-step plus the
+ *     wider halos.  Results are bit-identical to variant 0.  Psi^{n+1} is written to the T_A
+ *     workspace on odd steps and copied back once per call.  2D/3D single-slab handles only
+ *     (EUNSUPPORTED otherwise).
  * Variants 1 and 3 are 2SHOC forms: EUNSUPPORTED with the CD scheme.
  * EINVAL for other values.                                                             */
 nlse2shoc_status nlse2shoc_set_variant(nlse2shoc_t, int variant);
