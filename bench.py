@@ -233,7 +233,7 @@ def run_ours(args):
     value = npts_global * args.steps / (ms / 1e3)
 
     # end-to-end through the public API with HOST buffers: H2D(Psi0) + rk4(K) + D2H(Psi)
-    out_host = torch.empty_like(host)
+    out_host = torch.empty(lshape, dtype=torch.complex64, pin_memory=True)  # empty_like would not pin
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     torch.cuda.synchronize()
