@@ -395,7 +395,11 @@ __global__ void NLSE_PAIR_BOUNDS(PLayout<DIMS, R>::NTHREADS)
           named_bar_sync(1, NT);
         }
       }
-      if (jin && leanA && gzj >= 2 && gzj <= NZ - 3) {
+#ifndef NLSE_PAIR_EXPT
+#define NLSE_PAIR_EXPT 0  // timing experiments only: 1 = skip phase A compute, 2 = skip phase B compute
+#endif
+      if (NLSE_PAIR_EXPT == 1) {
+      } else if (jin && leanA && gzj >= 2 && gzj <= NZ - 3) {
         const CT *s0 = islot(j), *sm1 = islot(j - 1), *sm2 = islot(j - 2), *sp1 = islot(j + 1), *sp2 = islot(j + 2);
         const CT *ps = B ? sslot(j) : nullptr;
         CT *md = mslot(j);
@@ -637,7 +641,8 @@ __global__ void NLSE_PAIR_BOUNDS(PLayout<DIMS, R>::NTHREADS)
           }
         }
         };
-        if (leanB && gz >= 2 && gz <= NZ - 3) bloop(std::true_type{});
+        if (NLSE_PAIR_EXPT == 2) {
+        } else if (leanB && gz >= 2 && gz <= NZ - 3) bloop(std::true_type{});
         else bloop(std::false_type{});
         outT += P.plane;
         if (!B) outA += P.plane;

@@ -717,7 +717,8 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
     // faces (no boundary point, no ghost): straight-line loads, arithmetic and stores.
     const CT *ringT = ring + toff;
     const int64_t pitch = P.pitch, plane = P.plane;
-    auto lean_step = [&](int k) {
+    auto lean_step = [&](int k, auto varr_c) {
+      constexpr bool VARR = decltype(varr_c)::value;  // array potential (else separable tables)
       const int gz = z0 + k;
       const R vzk = vz_next(k);
       mbar_wait(&fullT[sk2], ph2);
@@ -768,7 +769,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
             L = axpy(L, -cy, ym2[q] + yp2[q]);
           }
           R V;
-          if (P.vkind == 2) V = potential(P, x0 + lx0 + q, y0 + ly0 + r, k);
+          if (VARR) V = potential(P, x0 + lx0 + q, y0 + ly0 + r, k);
           else V = (vxr[q] + vyr[r]) + vzk;
           const R N = fma(ps_, norm2(c), -V);
           const CT tF = axpy(N * c, pa_, L);  // F = i (a L + N c)
@@ -832,7 +833,17 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
       const int l0 = min(ke, max(kb, 2 - z0)), l1 = max(l0, min(ke, NZ - 2 - z0));
       int k = kb;
       for (; k < l0; ++k) general_step(k);
-      for (; k < l1; ++k) lean_step(k);
+#ifndef NLSE_LEAN_UNROLL
+#define NLSE_LEAN_UNROLL 1
+#endif
+      constexpr int kLU = NLSE_LEAN_UNROLL;
+      if (P.vkind == 2) {
+#pragma unroll (kLU)
+        for (; k < l1; ++k) lean_step(k, std::true_type{});
+      } else {
+#pragma unroll (kLU)
+        for (; k < l1; ++k) lean_step(k, std::false_type{});
+      }
       for (; k < ke; ++k) general_step(k);
     } else {
       for (int k = kb; k < ke; ++k) general_step(k);
