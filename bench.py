@@ -124,10 +124,37 @@ def oracle_sample(work, steps_per_call, box=96):
 
 
 def cores():
+    """OpenMP threads the oracle actually runs with."""
+    import oracle
+
+    return oracle.set_threads(0)
+
+
+def host_info():
+    """CPU model, sockets and logical CPUs of the box the oracle runs on."""
+    model, sockets = None, set()
     try:
-        return int(os.environ.get("OMP_NUM_THREADS", "")) or os.cpu_count()
-    except ValueError:
-        return os.cpu_count()
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name") and model is None:
+                model = ln.split(":", 1)[1].strip()
+            elif ln.startswith("physical id"):
+                sockets.add(ln.split(":", 1)[1].strip())
+    except OSError:
+        pass
+    return {"cpu_model": model, "sockets": len(sockets) or None, "nproc": os.cpu_count()}
+
+
+def cpu_baseline_line(work, box):
+    """The oracle on all host cores (box^3 sample) and on one core (a smaller sample)."""
+    import oracle
+
+    nth = oracle.set_threads(0)
+    pts, tcpu, desc = oracle_sample(work, 1, box=box)
+    oracle.set_threads(1)
+    p1, t1, d1 = oracle_sample(work, 1, box=max(16, box // 2))
+    oracle.set_threads(nth)
+    return {"value": pts / tcpu, "unit": UNIT, "cores": nth, "kind": "oracle", "sample": desc,
+            "value_1core": p1 / t1, "sample_1core": d1, **host_info()}
 
 
 def run_reference(args):
@@ -158,7 +185,8 @@ def run_reference(args):
             "impl": "reference",
             "config": {"workload": "C4_vortex_ring_3d (BASELINE configs[3]) sample", "grid": [768, 768, 768],
                        "sample": desc},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores(), "kind": "oracle", "sample": desc},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores(), "kind": "oracle", "sample": desc,
+                             **host_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     if ws > 1:
@@ -287,9 +315,7 @@ def run_ours(args):
             "clocks": clocks,
         }
         if ws == 1 and not args.no_cpu_baseline:
-            pts, tcpu, desc = oracle_sample(work, 1, box=int(os.environ.get("NLSE_REF_BOX", "96")))
-            line["cpu_baseline"] = {"value": pts / tcpu, "unit": UNIT, "cores": cores(), "kind": "oracle",
-                                    "sample": desc}
+            line["cpu_baseline"] = cpu_baseline_line(work, int(os.environ.get("NLSE_REF_BOX", "96")))
         print(json.dumps(line), flush=True)
     S.close()
     if dist is not None:

@@ -74,6 +74,8 @@ def _load():
         lib.orc_kmax.argtypes = [P, ctypes.c_void_p]
         lib.orc_table2_G.restype = ctypes.c_int
         lib.orc_table2_G.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+        lib.orc_set_threads.restype = ctypes.c_int
+        lib.orc_set_threads.argtypes = [ctypes.c_int]
         _lib = lib
     return _lib
 
@@ -179,3 +181,8 @@ def problem_from_work(work: dict, scheme: str = "2shoc", lo=None, cnt=None) -> P
     if work["V"]["kind"] in ("harmonic", "array"):
         V = icgen.harmonic(g, work["V"]["w"], work["V"]["c"], lo=lo, cnt=cnt)
     return Problem(dims, cnt[:dims], g["h"][:dims], work["a"], work["s"], V, work["bc"], scheme)
+
+
+def set_threads(n: int = 0) -> int:
+    """OpenMP threads of the oracle's point loops (n > 0 sets them); returns the count in effect."""
+    return int(_load().orc_set_threads(int(n)))

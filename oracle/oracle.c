@@ -352,3 +352,10 @@ double orc_kmax(const orc_problem *P, const double *psi) {
   if (orc_N_minmax(P, psi, &lo, &hi)) return -1.0;
   return orc_kmax_from_N(P->dims, P->h, P->a, lo, hi);
 }
+
+/* Test-infrastructure knob (no arithmetic): OpenMP threads for the oracle's point loops.
+ * n > 0 sets the count; returns the count now in effect. */
+int orc_set_threads(int n) {
+  if (n > 0) omp_set_num_threads(n);
+  return omp_get_max_threads();
+}

@@ -65,6 +65,9 @@ double orc_kmax_from_N(int dims, const double h[3], double a, double nmin, doubl
 double orc_kmax(const orc_problem *P, const double *psi);
 /* The G set of Table 2 for d (1..3), in units of 1/12; returns its size. */
 int orc_table2_G(int d, int *out12);
+/* Test-infrastructure knob: OpenMP threads of the point loops (n > 0 sets); returns the count
+ * in effect. */
+int orc_set_threads(int n);
 
 #ifdef __cplusplus
 }
