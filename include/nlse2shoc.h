@@ -175,6 +175,18 @@ nlse2shoc_status nlse2shoc_check_finite(nlse2shoc_t, const void *psi, void *stre
 /* Number of CUDA kernels the last laplacian / rk4 call enqueued (instrumentation). */
 int64_t nlse2shoc_last_launch_count(nlse2shoc_t);
 
+/* Device allocator for every buffer the library owns (workspace fields, halos, tables, D).
+ * Process-wide; captured by each handle at create and used until its destroy, so a handle
+ * always frees with the allocator it allocated with.  alloc(bytes, device, ctx) returns a
+ * device pointer aligned to >= 256 B, or NULL (-> ENOMEM); free(ptr, device, ctx) releases it.
+ * Both NULL restores cudaMalloc/cudaFree.  The Python binding installs torch's caching
+ * allocator here, so all device memory is PyTorch's (north star: "PyTorch used only for
+ * device memory, streams and process groups").  NCCL's internal buffers are NCCL's own.
+ * EINVAL if exactly one of alloc / free is NULL.                                          */
+typedef void *(*nlse2shoc_alloc_fn)(size_t bytes, int device, void *ctx);
+typedef void (*nlse2shoc_free_fn)(void *ptr, int device, void *ctx);
+nlse2shoc_status nlse2shoc_set_allocator(nlse2shoc_alloc_fn alloc, nlse2shoc_free_fn free_fn, void *ctx);
+
 const char *nlse2shoc_strerror(nlse2shoc_status);
 const char *nlse2shoc_last_error(void);
 /* Library version string, e.g. "nlse2shoc 0.1 sm_100a nccl". */

@@ -84,8 +84,50 @@ def lib():
         L.nlse2shoc_version.restype = ctypes.c_char_p
         L.nlse2shoc_destroy.argtypes = [H]
         L.nlse2shoc_destroy.restype = None
+        L.nlse2shoc_set_allocator.argtypes = [ALLOC_FN, FREE_FN, ctypes.c_void_p]
+        L.nlse2shoc_set_allocator.restype = ctypes.c_int
         _lib = L
+        if os.environ.get("NLSE_CUDA_MALLOC") != "1":
+            use_torch_allocator()
     return _lib
+
+
+# All device memory the library owns comes from torch's caching allocator (north star:
+# PyTorch for device memory).  NLSE_CUDA_MALLOC=1 keeps the library's own cudaMalloc.
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p)
+FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p)
+
+
+def _torch_alloc(nbytes, device, ctx):
+    try:
+        import torch
+
+        return int(torch.cuda.caching_allocator_alloc(int(nbytes), device=int(device)))
+    except Exception:  # out of memory (or torch unusable): the library reports ENOMEM
+        return None
+
+
+def _torch_free(ptr, device, ctx):
+    try:
+        import torch
+
+        torch.cuda.caching_allocator_delete(int(ptr))
+    except Exception:  # interpreter shutdown
+        pass
+
+
+_ALLOC_CB = ALLOC_FN(_torch_alloc)
+_FREE_CB = FREE_FN(_torch_free)
+
+
+def use_torch_allocator(enable: bool = True):
+    """Route the library's device allocations through torch (process-wide, for handles
+    created afterwards); enable=False restores cudaMalloc."""
+    L = lib()
+    if enable:
+        check(L.nlse2shoc_set_allocator(_ALLOC_CB, _FREE_CB, None), "set_allocator")
+    else:
+        check(L.nlse2shoc_set_allocator(ALLOC_FN(), FREE_FN(), None), "set_allocator")
 
 
 def check(status, where):
@@ -103,4 +145,5 @@ EXPORTS = [
     "nlse2shoc_split", "nlse2shoc_workspace_bytes", "nlse2shoc_set_variant", "nlse2shoc_set_scheme", "nlse2shoc_laplacian",
     "nlse2shoc_rk4", "nlse2shoc_stability_bound", "nlse2shoc_check_finite", "nlse2shoc_last_launch_count",
     "nlse2shoc_strerror", "nlse2shoc_last_error", "nlse2shoc_version", "nlse2shoc_destroy",
+    "nlse2shoc_set_allocator",
 ]

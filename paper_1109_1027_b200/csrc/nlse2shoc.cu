@@ -82,6 +82,9 @@ struct nlse2shoc_s {
   nlse2shoc_potential V{};
   int bc = 0, dtype = 0, device = 0, variant = 0, scheme = 0;
   int D_fields = 0;  // D fields allocated for the two-kernel variants
+  nlse2shoc_alloc_fn alloc = nullptr;  // device allocator captured at create (null: cudaMalloc)
+  nlse2shoc_free_fn dfree = nullptr;
+  void *alloc_ctx = nullptr;
   size_t S = 8;  // bytes per complex
   // slab (streamed axis = dims-1)
   int rank = 0, nranks = 1;
@@ -112,6 +115,34 @@ struct nlse2shoc_s {
   ncclComm_t comm = nullptr;
 #endif
 };
+
+// Device allocator: cudaMalloc, or the caller's (e.g. torch's caching allocator) when set
+// through nlse2shoc_set_allocator before create.
+static nlse2shoc_alloc_fn g_alloc = nullptr;
+static nlse2shoc_free_fn g_free = nullptr;
+static void *g_alloc_ctx = nullptr;
+
+template <typename T> static cudaError_t dev_malloc(nlse2shoc_t H, T **p, size_t n) {
+  if (H->alloc) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    void *q = H->alloc(n, dev, H->alloc_ctx);
+    *p = reinterpret_cast<T *>(q);
+    return q ? cudaSuccess : cudaErrorMemoryAllocation;
+  }
+  return cudaMalloc(reinterpret_cast<void **>(p), n);
+}
+
+static cudaError_t dev_free(nlse2shoc_t H, void *p) {
+  if (!p) return cudaSuccess;
+  if (H->dfree) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    H->dfree(p, dev, H->alloc_ctx);
+    return cudaSuccess;
+  }
+  return cudaFree(p);
+}
 
 static const char *kErr[] = {"ok", "invalid argument", "out of device memory", "CUDA error", "NCCL error",
                              "non-finite value", "unsupported"};
@@ -287,14 +318,14 @@ static nlse2shoc_status launch_stream(nlse2shoc_t H, Field &in, const CUtensorMa
   static const int lead = getenv("NLSE_LEAD") ? atoi(getenv("NLSE_LEAD")) : 0;
   static const int rbar = getenv("NLSE_RBAR") ? atoi(getenv("NLSE_RBAR")) : 0;
   if (rbar && P.ntiles > G) {
-    if (!H->rbar) CUDA_TRY(cudaMalloc(&H->rbar, 256));
+    if (!H->rbar) CUDA_TRY(dev_malloc(H, &H->rbar, 256));
     CUDA_TRY(cudaMemsetAsync(H->rbar, 0, sizeof(uint32_t), st));
     P.rbar = H->rbar;
   }
   if (lead > 0) {
     if (H->prog_cap < P.ntiles) {
-      if (H->prog) cudaFree(H->prog);
-      CUDA_TRY(cudaMalloc(&H->prog, sizeof(uint32_t) * P.ntiles));
+      if (H->prog) dev_free(H, H->prog);
+      CUDA_TRY(dev_malloc(H, &H->prog, sizeof(uint32_t) * P.ntiles));
       CUDA_TRY(cudaMemsetAsync(H->prog, 0, sizeof(uint32_t) * P.ntiles, st));
       H->prog_cap = P.ntiles;
     }
@@ -589,12 +620,12 @@ static nlse2shoc_status run_rk4(View &v, double dt, int64_t nsteps, cudaStream_t
 // ------------------------------------------------------------------------------ create
 static nlse2shoc_status alloc_field(nlse2shoc_t H, Field &f, bool halos) {
   const size_t bytes = size_t(H->local_elems) * H->S;
-  CUDA_TRY(cudaMalloc(&f.ptr, bytes));
+  CUDA_TRY(dev_malloc(H, &f.ptr, bytes));
   H->bytes += bytes;
   if (halos && H->sharded) {
     const size_t hb = size_t(2 * H->plane) * H->S;
-    CUDA_TRY(cudaMalloc(&f.halo_lo, hb));
-    CUDA_TRY(cudaMalloc(&f.halo_hi, hb));
+    CUDA_TRY(dev_malloc(H, &f.halo_lo, hb));
+    CUDA_TRY(dev_malloc(H, &f.halo_hi, hb));
     CUDA_TRY(cudaMemsetAsync(f.halo_lo, 0, hb));
     CUDA_TRY(cudaMemsetAsync(f.halo_hi, 0, hb));
     H->bytes += 2 * hb;
@@ -687,6 +718,9 @@ static nlse2shoc_status create_impl(nlse2shoc_t *out, int dims, const int64_t N[
 #endif
 
   auto *H = new nlse2shoc_s();
+  H->alloc = g_alloc;
+  H->dfree = g_free;
+  H->alloc_ctx = g_alloc_ctx;
   H->dims = dims;
   for (int d = 0; d < 3; ++d) { H->N[d] = N[d]; H->h[d] = d < dims ? h[d] : 1.0; }
   H->a = a;
@@ -730,7 +764,7 @@ static nlse2shoc_status create_impl(nlse2shoc_t *out, int dims, const int64_t N[
     }
     if (st == NLSE2SHOC_OK && H->pitch != H->nx) {
       chk(alloc_field(H, H->psiw, false));
-      if (st == NLSE2SHOC_OK && cudaMalloc(&H->Lw, size_t(H->local_elems) * H->S) != cudaSuccess)
+      if (st == NLSE2SHOC_OK && dev_malloc(H, &H->Lw, size_t(H->local_elems) * H->S) != cudaSuccess)
         chk(fail(NLSE2SHOC_ENOMEM, "staging allocation failed"));
     }
     if (st != NLSE2SHOC_OK) {
@@ -746,13 +780,13 @@ static nlse2shoc_status create_impl(nlse2shoc_t *out, int dims, const int64_t N[
   chk(alloc_field(H, H->acc, false));
   if (st == NLSE2SHOC_OK && H->pitch != H->nx && !H->loop_member) {
     chk(alloc_field(H, H->psiw, true));
-    if (st == NLSE2SHOC_OK && cudaMalloc(&H->Lw, size_t(H->local_elems) * H->S) != cudaSuccess)
+    if (st == NLSE2SHOC_OK && dev_malloc(H, &H->Lw, size_t(H->local_elems) * H->S) != cudaSuccess)
       chk(fail(NLSE2SHOC_ENOMEM, "staging allocation failed"));
   }
   if (st == NLSE2SHOC_OK && H->sharded && (H->pitch == H->nx || H->loop_member)) {
     // halo buffers for the caller's Psi (zero-copy path)
     const size_t hb = size_t(2 * H->plane) * H->S;
-    if (cudaMalloc(&H->psiw.halo_lo, hb) != cudaSuccess || cudaMalloc(&H->psiw.halo_hi, hb) != cudaSuccess)
+    if (dev_malloc(H, &H->psiw.halo_lo, hb) != cudaSuccess || dev_malloc(H, &H->psiw.halo_hi, hb) != cudaSuccess)
       chk(fail(NLSE2SHOC_ENOMEM, "halo allocation failed"));
     H->bytes += 2 * hb;
   }
@@ -766,14 +800,14 @@ static nlse2shoc_status create_impl(nlse2shoc_t *out, int dims, const int64_t N[
     std::vector<unsigned char> host;
     if (dtype == NLSE2SHOC_C64) build_tables<float>(H, host);
     else build_tables<double>(H, host);
-    if (cudaMalloc(&H->vtab, host.size()) != cudaSuccess) chk(fail(NLSE2SHOC_ENOMEM, "table allocation failed"));
+    if (dev_malloc(H, &H->vtab, host.size()) != cudaSuccess) chk(fail(NLSE2SHOC_ENOMEM, "table allocation failed"));
     else if (cudaMemcpy(H->vtab, host.data(), host.size(), cudaMemcpyHostToDevice) != cudaSuccess)
       chk(fail(NLSE2SHOC_ECUDA, "table upload failed"));
     H->bytes += host.size();
   }
   if (st == NLSE2SHOC_OK) {
     H->red_blocks = H->num_sms * 4;
-    if (cudaMalloc(&H->red, sizeof(double) * 3 * H->red_blocks) != cudaSuccess)
+    if (dev_malloc(H, &H->red, sizeof(double) * 3 * H->red_blocks) != cudaSuccess)
       chk(fail(NLSE2SHOC_ENOMEM, "reduction buffer allocation failed"));
   }
 #ifdef NLSE_WITH_NCCL
@@ -867,12 +901,12 @@ static nlse2shoc_status ensure_D(nlse2shoc_t H, int nfields) {
   if (H->D.ptr && H->D_fields >= nfields) return NLSE2SHOC_OK;
   const size_t bytes = size_t(D_field_elems(H)) * H->S;
   if (H->D.ptr) {
-    CUDA_TRY(cudaFree(H->D.ptr));
+    CUDA_TRY(dev_free(H, H->D.ptr));
     H->D.ptr = nullptr;
     H->bytes -= bytes * size_t(H->D_fields);
     H->D_fields = 0;
   }
-  CUDA_TRY(cudaMalloc(&H->D.ptr, bytes * size_t(nfields)));
+  CUDA_TRY(dev_malloc(H, &H->D.ptr, bytes * size_t(nfields)));
   H->bytes += bytes * size_t(nfields);
   H->D_fields = nfields;
   return NLSE2SHOC_OK;
@@ -1087,6 +1121,14 @@ int64_t nlse2shoc_last_launch_count(nlse2shoc_t H) {
   return n;
 }
 
+nlse2shoc_status nlse2shoc_set_allocator(nlse2shoc_alloc_fn alloc, nlse2shoc_free_fn free_fn, void *ctx) {
+  if ((alloc == nullptr) != (free_fn == nullptr)) return fail(NLSE2SHOC_EINVAL, "alloc and free must both be set or both NULL");
+  g_alloc = alloc;
+  g_free = free_fn;
+  g_alloc_ctx = ctx;
+  return NLSE2SHOC_OK;
+}
+
 const char *nlse2shoc_strerror(nlse2shoc_status st) {
   const int i = -int(st);
   if (i < 0 || i > 6) return "unknown status";
@@ -1107,16 +1149,16 @@ void nlse2shoc_destroy(nlse2shoc_t H) {
   if (!H) return;
   cudaDeviceSynchronize();
   for (nlse2shoc_t S : H->slabs) nlse2shoc_destroy(S);
-  if (H->Lw) cudaFree(H->Lw);
+  if (H->Lw) dev_free(H, H->Lw);
   for (Field *f : {&H->TA, &H->TB, &H->acc, &H->psiw, &H->D}) {
-    if (f->ptr) cudaFree(f->ptr);
-    if (f->halo_lo) cudaFree(f->halo_lo);
-    if (f->halo_hi) cudaFree(f->halo_hi);
+    if (f->ptr) dev_free(H, f->ptr);
+    if (f->halo_lo) dev_free(H, f->halo_lo);
+    if (f->halo_hi) dev_free(H, f->halo_hi);
   }
-  if (H->vtab) cudaFree(H->vtab);
-  if (H->prog) cudaFree(H->prog);
-  if (H->rbar) cudaFree(H->rbar);
-  if (H->red) cudaFree(H->red);
+  if (H->vtab) dev_free(H, H->vtab);
+  if (H->prog) dev_free(H, H->prog);
+  if (H->rbar) dev_free(H, H->rbar);
+  if (H->red) dev_free(H, H->red);
 #ifdef NLSE_WITH_NCCL
   if (H->comm) ncclCommDestroy(H->comm);
 #endif

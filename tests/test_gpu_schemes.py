@@ -205,3 +205,20 @@ def test_stage_pairs_full_C4_grid_vs_per_stage(dtype):
     assert torch.equal(res[4][0], psi0[0]) and torch.equal(res[4][:, :, -1], psi0[:, :, -1])
     # same expressions in the same order in both kernels: the results agree bit for bit
     assert torch.equal(res[4], res[0])
+
+
+def test_workspace_comes_from_torch_allocator():
+    """The binding installs torch's caching allocator (nlse2shoc_set_allocator): the handle's
+    workspace shows up in torch.cuda.memory_allocated and goes back on close."""
+    w = configs.SMALL(3, (70, 35, 11), "dirichlet", "c64")
+    torch.cuda.synchronize()
+    before = torch.cuda.memory_allocated()
+    S = H.gpu_solver(w, "c64")
+    during = torch.cuda.memory_allocated()
+    assert during - before >= S.workspace_bytes
+    g = _dev(H.psi0_host(w, "c64"))
+    S.rk4(g, 1e-4, 2)
+    assert torch.isfinite(torch.view_as_real(g)).all()
+    S.close()
+    torch.cuda.synchronize()
+    assert torch.cuda.memory_allocated() <= before + g.numel() * 8 + 512  # allocator rounding
