@@ -259,25 +259,42 @@ __global__ void NLSE_PAIR_BOUNDS(PLayout<DIMS, R>::NTHREADS)
     const int x0 = (col % P.ncx) * TX, y0 = (col / P.ncx) * TY;
     const int kb = chunk * chunk_len, ke = min(nz, kb + chunk_len);
     const uint32_t ib = icnt, sb = scnt, ab = acnt, mb = mcnt;  // counters of planes kb-4, kb-2, kb, kb-2
-    auto islot = [&](int p) -> CT * { return iring + size_t((ib + uint32_t(p - kb + 4)) % RI) * LY::ISLOT; };
-    auto sslot = [&](int p) -> CT * { return sring + size_t((sb + uint32_t(p - kb + 2)) % RPSM) * LY::ESLOT; };
+    // Ring positions advance by one slot per plane iteration (no divisions in the plane loop):
+    // jc = current plane j; bI = input slot of plane jc-2; sJ = Psi slot of plane jc; mJ = mid
+    // slot of plane jc; (s4, par4) = input slot and phase of plane jc+2; sPar = phase of sJ.
+    int jc = kb - 2;
+    int bI = int(ib % RI), sJ = int(sb % RPSM), mJ = int(mb % RM);
+    int s4 = int((ib + 4) % RI);
+    uint32_t par4 = ((ib + 4) / RI) & 1u, sPar = (sb / RPSM) & 1u;
+    auto islot = [&](int p) -> CT * {  // p in [jc-2, jc+2]
+      int q = bI + (p - jc + 2);
+      q = q >= RI ? q - RI : q;
+      return iring + size_t(q) * LY::ISLOT;
+    };
+    auto sslot = [&](int p) -> CT * {  // p in [jc-2, jc]
+      int q = sJ + (p - jc);
+      q = q < 0 ? q + RPSM : q;
+      return sring + size_t(q) * LY::ESLOT;
+    };
     auto aslot = [&](int p) -> CT * { return aring + size_t((ab + uint32_t(p - kb)) % RAM) * LY::PTILE; };
-    auto mslot = [&](int p) -> CT * { return mring + size_t((mb + uint32_t(p - kb + 2)) % RM) * LY::ESLOT; };
-    auto iwait = [&](int p) {
+    auto mslot = [&](int p) -> CT * {  // p in [jc-4, jc]
+      int q = mJ + (p - jc);
+      q = q < 0 ? q + RM : q;
+      return mring + size_t(q) * LY::ESLOT;
+    };
+    auto iwait0 = [&](int p) {  // tile start only
       const uint32_t c = ib + uint32_t(p - kb + 4);
       mbar_wait(&fullI[c % RI], (c / RI) & 1);
     };
-    auto irelease = [&](int p) {
-      const uint32_t c = ib + uint32_t(p - kb + 4);
-      if (lane == 0) mbar_arrive(&emptyI[c % RI]);
+    auto irelease = [&](int p) {  // p in [jc-2, jc+1]
+      int q = bI + (p - jc + 2);
+      q = q >= RI ? q - RI : q;
+      if (lane == 0) mbar_arrive(&emptyI[q]);
     };
-    auto swait = [&](int p) {
-      const uint32_t c = sb + uint32_t(p - kb + 2);
-      mbar_wait(&fullS[c % RPSM], (c / RPSM) & 1);
-    };
-    auto srelease = [&](int p) {
-      const uint32_t c = sb + uint32_t(p - kb + 2);
-      if (lane == 0) mbar_arrive(&emptyS[c % RPSM]);
+    auto srelease = [&](int p) {  // p in [jc-2, jc]
+      int q = sJ + (p - jc);
+      q = q < 0 ? q + RPSM : q;
+      if (lane == 0) mbar_arrive(&emptyS[q]);
     };
     // input slot position of tile-relative (lx, ly); ext/mid slot position
     auto ati = [&](CT *s, int lx, int ly) -> CT & { return s[(ly + HI) * WI + lx + 4]; };
@@ -328,10 +345,10 @@ __global__ void NLSE_PAIR_BOUNDS(PLayout<DIMS, R>::NTHREADS)
     cplx<R> *outT = P.out_T + int64_t(kb) * P.plane + int64_t(y0 + ly0) * P.pitch + (x0 + lx0);
     cplx<R> *outA = B ? nullptr : P.out_acc + (outT - P.out_T);
 
-    for (int p = kb - 4; p < kb; ++p) iwait(p);
+    for (int p = kb - 4; p < kb; ++p) iwait0(p);
     for (int j = kb - 2; j < ke + 2; ++j) {
-      iwait(j + 2);
-      if (B) swait(j);
+      mbar_wait(&fullI[s4], par4);  // input plane j+2
+      if (B) mbar_wait(&fullS[sJ], sPar);  // Psi plane j
       const int gzj = z0 + j;
       const bool jin = j >= 0 && j < nz;
       if (j == kb + 2) {
@@ -656,6 +673,18 @@ __global__ void NLSE_PAIR_BOUNDS(PLayout<DIMS, R>::NTHREADS)
       __syncwarp();
       irelease(j - 2);
       if (B && j - 2 >= kb - 2) srelease(j - 2);
+      // advance the ring positions to plane j+1
+      ++jc;
+      bI = bI + 1 == RI ? 0 : bI + 1;
+      mJ = mJ + 1 == RM ? 0 : mJ + 1;
+      if (++s4 == RI) {
+        s4 = 0;
+        par4 ^= 1u;
+      }
+      if (++sJ == RPSM) {
+        sJ = 0;
+        sPar ^= 1u;
+      }
     }
     __syncwarp();
     for (int p = ke; p < ke + 4; ++p) irelease(p);
