@@ -97,6 +97,61 @@ __global__ void __launch_bounds__(256) stage_line_kernel(const cplx<R> *__restri
   }
 }
 
+// 1D stage over tiles of 256 * PT points staged in shared memory (coalesced loads, one read
+// per point plus a 4-point halo per tile, conflict-free strided reads); the two points at each
+// grid end (ghost / MSD rules) go through line_point on global memory.  Same arithmetic as
+// stage_line_kernel.
+template <typename R, int MODE, int PT>
+__global__ void __launch_bounds__(256) line_tile_kernel(const cplx<R> *__restrict__ Tin, const cplx<R> *__restrict__ psi,
+                                                        const cplx<R> *__restrict__ acc, const StageParams<R> P) {
+  using CT = cplx<R>;
+  constexpr int TILE = 256 * PT;
+  __shared__ __align__(16) CT sT[TILE + 8];  // sT[k] = Tin[t0 - 4 + k]
+  const int n = P.nx;
+  const int64_t t0 = int64_t(blockIdx.x) * TILE;
+  for (int k = threadIdx.x; k < TILE + 8; k += 256) {
+    const int64_t g = t0 - 4 + k;
+    sT[k] = (g >= 0 && g < n) ? Tin[g] : mk<R>(R(0), R(0));
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < PT; ++q) {
+    const int64_t i = t0 + q * 256 + threadIdx.x;
+    if (i >= n) break;
+    CT c, L, t;
+    if (i < 2 || i >= n - 2) {
+      t = line_point(Tin, i, n, P, c, L);
+    } else {
+      const CT *pp = sT + (i - t0 + 4);
+      c = pp[0];
+      L = axpy(axpy((-P.c30) * c, P.c1x, pp[-1] + pp[1]), -P.cx, pp[-2] + pp[2]);
+      const R N = fma(P.s, norm2(c), -potential(P, int(i), 0, 0));
+      t = axpy(N * c, P.a, L);
+    }
+    if (MODE == M_LAP) {
+      P.out_T[i] = L;
+    } else if (MODE == M_S1) {
+      P.out_acc[i] = iaxpy(c, P.ca, t);
+      P.out_T[i] = iaxpy(c, P.cb, t);
+    } else if (MODE == M_S1R) {
+      P.out_T[i] = iaxpy(c, P.cb, t);
+    } else if (MODE == M_S2R) {
+      const CT ps = psi[i];
+      P.out_acc[i] = iaxpy(axpy(ps, R(1.0 / 3.0), c - ps), P.ca, t);
+      P.out_T[i] = iaxpy(ps, P.cb, t);
+    } else if (MODE == M_S3R) {
+      P.out_T[i] = iaxpy(psi[i], P.cb, t);
+    } else if (MODE == M_S4R) {
+      P.out_T[i] = iaxpy(axpy(acc[i], R(1.0 / 3.0), c - psi[i]), P.cb, t);
+    } else if (MODE == M_S2 || MODE == M_S3) {
+      P.out_acc[i] = iaxpy(acc[i], P.ca, t);
+      P.out_T[i] = iaxpy(psi[i], P.cb, t);
+    } else {
+      P.out_T[i] = iaxpy(acc[i], P.cb, t);
+    }
+  }
+}
+
 // Resident small-grid 1D solver: the whole grid (Psi, T_A, T_B, acc) lives in one CTA's
 // shared memory and the CTA runs all nsteps x 4 stages of an nlse2shoc_rk4 call, separated
 // by barriers.  Same per-point arithmetic as stage_line_kernel; one launch per call instead
