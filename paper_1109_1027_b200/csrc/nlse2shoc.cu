@@ -598,10 +598,14 @@ template <typename R> static nlse2shoc_status rk4_resident_1d(nlse2shoc_t H, Fie
   const size_t smem = size_t(4) * size_t(H->nx) * sizeof(cplx<R>);
   static bool attr = false;
   if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(resident_line_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CUDA_TRY(cudaFuncSetAttribute(resident_line_kernel<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CUDA_TRY(cudaFuncSetAttribute(resident_line_kernel<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
-  resident_line_kernel<R><<<1, 1024, smem, st>>>(reinterpret_cast<cplx<R> *>(psi.ptr), nsteps, R(dt), P);
+  if (H->bc == NLSE2SHOC_BC_MSD)
+    resident_line_kernel<R, true><<<1, 1024, smem, st>>>(reinterpret_cast<cplx<R> *>(psi.ptr), nsteps, R(dt), P);
+  else
+    resident_line_kernel<R, false><<<1, 1024, smem, st>>>(reinterpret_cast<cplx<R> *>(psi.ptr), nsteps, R(dt), P);
   CUDA_TRY(cudaGetLastError());
   ++H->launches;
   return NLSE2SHOC_OK;

@@ -22,15 +22,16 @@ __device__ __forceinline__ cplx<R> msd_lambda(const cplx<R> *__restrict__ Tin, i
   return (re + (Nq - Nb) * P.inv_a) * cb;
 }
 
-template <typename R>
+// MSD = false compiles the MSD branches out (handles with another BC).
+template <typename R, bool MSD = true>
 __device__ __forceinline__ cplx<R> line_lambda(const cplx<R> *__restrict__ Tin, int b, int n, const StageParams<R> &P) {
-  if (P.bc == 2) return msd_lambda(Tin, b, b == 0 ? 1 : n - 2, P);
+  if (MSD && P.bc == 2) return msd_lambda(Tin, b, b == 0 ? 1 : n - 2, P);
   return lambda_b(P, Tin[b], potential(P, b, 0, 0));
 }
 
 // Interior point i of the 1D stage: the 5-point wide form with ghost values at the ends
 // (ghost = h^2 lambda_b + 2 Psi_b - Psi_{b+n}); returns t with F = i t.
-template <typename R>
+template <typename R, bool MSD = true>
 __device__ __forceinline__ cplx<R> line_interior(const cplx<R> *__restrict__ Tin, int64_t i, int n,
                                                 const StageParams<R> &P, cplx<R> &c, cplx<R> &L) {
   using CT = cplx<R>;
@@ -38,27 +39,27 @@ __device__ __forceinline__ cplx<R> line_interior(const cplx<R> *__restrict__ Tin
   const CT m1 = Tin[i - 1], p1 = Tin[i + 1];
   CT m2, p2;
   if (i >= 2) m2 = Tin[i - 2];
-  else m2 = axpy(R(2) * m1 - c, P.hx2, line_lambda(Tin, 0, n, P));
+  else m2 = axpy(R(2) * m1 - c, P.hx2, line_lambda<R, MSD>(Tin, 0, n, P));
   if (i <= n - 3) p2 = Tin[i + 2];
-  else p2 = axpy(R(2) * p1 - c, P.hx2, line_lambda(Tin, n - 1, n, P));
+  else p2 = axpy(R(2) * p1 - c, P.hx2, line_lambda<R, MSD>(Tin, n - 1, n, P));
   L = axpy(axpy((-P.c30) * c, P.c1x, m1 + p1), -P.cx, m2 + p2);  // 2SHOC wide form, or CD (cx = 0)
   const R N = fma(P.s, norm2(c), -potential(P, int(i), 0, 0));
   return axpy(N * c, P.a, L);  // a L + N c
 }
 
 // One point of the 1D stage: returns t with F = i t (and L for the Laplacian output).
-template <typename R>
+template <typename R, bool MSD = true>
 __device__ __forceinline__ cplx<R> line_point(const cplx<R> *__restrict__ Tin, int64_t i, int n, const StageParams<R> &P,
                                              cplx<R> &c, cplx<R> &L) {
   using CT = cplx<R>;
-  if (i != 0 && i != n - 1) return line_interior(Tin, i, n, P, c, L);
+  if (i != 0 && i != n - 1) return line_interior<R, MSD>(Tin, i, n, P, c, L);
   c = Tin[i];
-  L = line_lambda(Tin, int(i), n, P);
-  if (P.bc == 2) {
+  L = line_lambda<R, MSD>(Tin, int(i), n, P);
+  if (MSD && P.bc == 2) {
     // `msdbc_ut`: Psi_t,b = i Im(Psi_t,q / Psi_q) Psi_b, i.e. t_b = Re(t_q / Psi_q) Psi_b
     const int q = i == 0 ? 1 : n - 2;
     CT cq, Lq;
-    const CT tq = line_interior(Tin, q, n, P, cq, Lq);
+    const CT tq = line_interior<R, MSD>(Tin, q, n, P, cq, Lq);
     return (fma(tq.re, cq.re, tq.im * cq.im) / norm2(cq)) * c;
   }
   const R N = fma(P.s, norm2(c), -potential(P, int(i), 0, 0));
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(256) line_tile_kernel(const cplx<R> *__restric
 // shared memory and the CTA runs all nsteps x 4 stages of an nlse2shoc_rk4 call, separated
 // by barriers.  Same per-point arithmetic as stage_line_kernel; one launch per call instead
 // of 4 per step (C1: 2000 steps on 1024 points is otherwise launch-latency bound).
-template <typename R>
+template <typename R, bool MSD>
 __global__ void __launch_bounds__(1024, 1) resident_line_kernel(cplx<R> *__restrict__ psi_g, int64_t nsteps, R dt,
                                                                 const StageParams<R> P) {
   using CT = cplx<R>;
@@ -169,28 +170,28 @@ __global__ void __launch_bounds__(1024, 1) resident_line_kernel(cplx<R> *__restr
   for (int64_t step = 0; step < nsteps; ++step) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) {  // stage 1
       CT c, L;
-      const CT t = line_point<R>(psi, i, n, P, c, L);
+      const CT t = line_point<R, MSD>(psi, i, n, P, c, L);
       acc[i] = iaxpy(c, c6, t);
       TA[i] = iaxpy(c, c2, t);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += blockDim.x) {  // stage 2
       CT c, L;
-      const CT t = line_point<R>(TA, i, n, P, c, L);
+      const CT t = line_point<R, MSD>(TA, i, n, P, c, L);
       acc[i] = iaxpy(acc[i], c3, t);
       TB[i] = iaxpy(psi[i], c2, t);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += blockDim.x) {  // stage 3
       CT c, L;
-      const CT t = line_point<R>(TB, i, n, P, c, L);
+      const CT t = line_point<R, MSD>(TB, i, n, P, c, L);
       acc[i] = iaxpy(acc[i], c3, t);
       TA[i] = iaxpy(psi[i], dt, t);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += blockDim.x) {  // stage 4
       CT c, L;
-      const CT t = line_point<R>(TA, i, n, P, c, L);
+      const CT t = line_point<R, MSD>(TA, i, n, P, c, L);
       psi[i] = iaxpy(acc[i], c6, t);
     }
     __syncthreads();

@@ -30,9 +30,9 @@ def run(work, dtype, steps, variant=0, synthetic=False):
     ms = e0.elapsed_time(e1)
     npts = int(np.prod(g["n"][:dims]))
     S_b = 8 if dtype == "c64" else 16
-    r = {"config": work["name"], "dtype": dtype, "variant": ["fused", "two_kernel"][variant], "grid": g["n"][:dims],
+    r = {"config": work["name"], "dtype": dtype, "variant": {0: "fused", 1: "two_kernel", 4: "stage_pairs"}[variant], "grid": g["n"][:dims],
          "steps": steps, "ms_per_step": ms / steps, "pt_steps_s": npts * steps / ms * 1e3,
-         "alg_GBs": npts * steps * 16 * S_b / ms / 1e6, "launches": S.last_launch_count}
+         "alg_GBs_13S": npts * steps * 13 * S_b / ms / 1e6, "launches": S.last_launch_count}
     S.close(); del psi; torch.cuda.empty_cache()
     return r
 
@@ -40,10 +40,12 @@ only = sys.argv[1:]
 jobs = [("C1", configs.C1(), "c128", 2000, False), ("C2", configs.C2(), "c128", 200, False), ("C2", configs.C2(), "c64", 200, False),
         ("C3", configs.C3(), "c128", 40, False), ("C4", configs.C4(), "c64", 50, False),
         ("C5W", configs.C5W(1), "c64", 50, False), ("C5W", configs.C5W(1), "c128", 50, False),
-        ("C5S", configs.C5(), "c64", 10, True), ("C4-2k", configs.C4(), "c64", 20, False)]
+        ("C5S", configs.C5(), "c64", 10, True), ("C4-2k", configs.C4(), "c64", 20, False),
+        ("C4-pairs", configs.C4(), "c64", 20, False), ("C3-pairs", configs.C3(), "c128", 20, False)]
 for name, w, dt, steps, syn in jobs:
     if only and name not in only: continue
     try:
-        print(json.dumps(run(w, dt, steps, 1 if name.endswith("2k") else 0, syn)), flush=True)
+        v = 1 if name.endswith("2k") else (4 if name.endswith("pairs") else 0)
+        print(json.dumps(run(w, dt, steps, v, syn)), flush=True)
     except Exception as e:
         print(json.dumps({"config": name, "dtype": dt, "error": str(e)[:300]}), flush=True)
