@@ -11,6 +11,7 @@ Here each realisation in the library is timed on one B200 at a paper-sized workl
   2k-1X     variant 1: the paper's single-storage two-step scheme, D stored (`2d2shocs1/2`)
   2k-MS     variant 3: the paper's multi-storage scheme, D_d per axis stored (`*2shocMs1/2`)
   CD        scheme CD through fused-13 (`uttmp`, the 2nd-order comparison scheme)
+  pairs     variant 4: two stages per pass (temporal blocking, stage_pair.cuh)
 
   python scripts/cost_tables.py                 # timing -> JSON lines on stdout
   python scripts/cost_tables.py --ncu           # 1 Laplacian + 1 RK4 step per row (run under ncu)
@@ -32,7 +33,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 ROWS = [("fused-13", 0, "2shoc"), ("fused-16", 2, "2shoc"), ("2k-1X", 1, "2shoc"), ("2k-MS", 3, "2shoc"),
-        ("CD", 0, "cd")]
+        ("CD", 0, "cd"), ("pairs", 4, "2shoc")]
 
 # paper's static counts (Tables 3-5): (Laplacian ops, Laplacian storage, RK4 ops, RK4 storage)
 PAPER = {
@@ -50,7 +51,7 @@ def workloads():
 
 
 def rows_for(dims):
-    return [r for r in ROWS if not (dims == 1 and r[1] == 3)]  # 1D: MS == 1X
+    return [r for r in ROWS if not (dims == 1 and r[1] in (3, 4))]  # 1D: MS == 1X; pairs are 2D/3D
 
 
 def run(ncu: bool, steps: int, reps: int, only):
@@ -129,7 +130,7 @@ def parse(csv_path, order_path):
         names[int(r[idi])] = r[ki].split("(")[0]
     ids = sorted(d)
     # launches that are not the library's (torch fills, reductions) are skipped by name
-    ids = [i for i in ids if any(k in names[i] for k in ("stage", "two_", "line", "resident"))]
+    ids = [i for i in ids if any(k in names[i] for k in ("stage", "two_", "line", "resident", "pair"))]
     pos = 0
     out = []
     for o in order:
