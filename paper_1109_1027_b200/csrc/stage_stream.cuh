@@ -49,14 +49,23 @@ enum Mode { M_S1 = 1, M_S2 = 2, M_S3 = 3, M_S4 = 4, M_LAP = 5, M_S1R = 6, M_S2R 
 template <int DIMS, typename R> struct Cfg;
 // Ring depths from a shared-memory budget: the T ring keeps the pinned window (planes
 // k-1..k+2) plus a prefetch depth, the P ring gets the rest.
+#ifndef NLSE_RING_BUDGET_KB
+#define NLSE_RING_BUDGET_KB 210
+#endif
+#ifndef NLSE_RT1_KB
+#define NLSE_RT1_KB 40
+#endif
+#ifndef NLSE_RT2_KB
+#define NLSE_RT2_KB 24
+#endif
 template <int SLOT_B, int PT_B> struct Rings {
-  static constexpr int BUDGET = 210 * 1024;
+  static constexpr int BUDGET = NLSE_RING_BUDGET_KB * 1024;
   static constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
   static constexpr int mn(int a, int b) { return a < b ? a : b; }
   static constexpr int RT0 = mn(24, BUDGET / SLOT_B);
-  static constexpr int RT1 = 4 + cdiv(40 * 1024, SLOT_B);
+  static constexpr int RT1 = 4 + cdiv(NLSE_RT1_KB * 1024, SLOT_B);
   static constexpr int RP1 = mn(12, (BUDGET - RT1 * SLOT_B) / PT_B);
-  static constexpr int RT2 = 4 + cdiv(24 * 1024, SLOT_B);
+  static constexpr int RT2 = 4 + cdiv(NLSE_RT2_KB * 1024, SLOT_B);
   static constexpr int RP2 = mn(8, (BUDGET - RT2 * SLOT_B) / (2 * PT_B));
   static_assert(RT0 >= 5 && RP1 >= 2 && RP2 >= 2, "shared-memory budget too small for the tile");
 };
