@@ -326,9 +326,14 @@ static nlse2shoc_status launch_stream(nlse2shoc_t H, Field &in, const CUtensorMa
   P.nchunk = best;
   P.ntiles = ncol * best;
   const int G = std::min(G0, P.ntiles);
+  // stages 2 and 4 walk the tiles backwards: the planes the previous stage wrote last are
+  // still in L2 when this stage starts (NLSE_NO_REV=1 disables)
+  static const bool no_rev = getenv("NLSE_NO_REV") != nullptr;
+  P.rev = (!no_rev && (MODE == M_S2 || MODE == M_S4 || MODE == M_S2R || MODE == M_S4R)) ? 1 : 0;
   // neighbour coupling (NLSE_LEAD=0 disables): per-tile progress words, epoch-tagged
   static const int lead = getenv("NLSE_LEAD") ? atoi(getenv("NLSE_LEAD")) : 0;
   static const int rbar = getenv("NLSE_RBAR") ? atoi(getenv("NLSE_RBAR")) : 0;
+  if (lead > 0 || rbar) P.rev = 0;  // the coupling experiments index neighbours in forward order
   if (rbar && P.ntiles > G) {
     if (!H->rbar) CUDA_TRY(dev_malloc(H, &H->rbar, 256));
     CUDA_TRY(cudaMemsetAsync(H->rbar, 0, sizeof(uint32_t), st));

@@ -178,6 +178,7 @@ template <typename R> struct StageParams {
   R a, s, inv_a;
   R ca, cb;              // stage-combine coefficients (acc, T)
   R cA;                  // phase-A coefficient of the stage-pair kernel (stage_pair.cuh)
+  int rev;               // traverse the tiles in reverse order (alternate stages: L2 reuse)
   int bc;                // 0 Dirichlet, 1 Laplacian-zero, 2 MSD (1D line kernels only)
   int vkind;             // 0 none, 1 harmonic tables, 2 array
   const R *vx, *vy, *vz; // harmonic tables (vz indexed by GLOBAL streamed index)
@@ -339,13 +340,14 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
 #define NLSE_TPOL 2
 #endif
 #ifndef NLSE_PPOL
-#define NLSE_PPOL 0
+#define NLSE_PPOL 1
 #endif
       const uint64_t pol_keep = NLSE_TPOL == 2 ? policy_evict_last() : (NLSE_TPOL == 1 ? policy_evict_normal() : policy_evict_first());
       const uint64_t pol_stream = NLSE_PPOL == 0 ? policy_evict_first() : policy_evict_normal();
       uint32_t tcnt = 0, pcnt = 0;
       for (int t = blockIdx.x; t < P.ntiles; t += G) {
-        const int chunk = t / ncol, col = t % ncol;
+        const int tt = P.rev ? P.ntiles - 1 - t : t;  // reversed order: read the L2-resident tail first
+        const int chunk = tt / ncol, col = tt % ncol;
         const int x0 = (col % P.ncx) * TX, y0 = (col / P.ncx) * TY;
         const int kb = chunk * chunk_len, ke = min(P.nz, kb + chunk_len);
         // Round barrier: every producer starts round r only after all producers finished
@@ -461,7 +463,8 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
   auto inc = [](int v, int m) { return v + 1 == m ? 0 : v + 1; };
 
   for (int t = blockIdx.x; t < P.ntiles; t += G) {
-    const int chunk = t / ncol, col = t % ncol;
+    const int tt = P.rev ? P.ntiles - 1 - t : t;
+    const int chunk = tt / ncol, col = tt % ncol;
     const int x0 = (col % P.ncx) * TX, y0 = (col / P.ncx) * TY;
     const int kb = chunk * chunk_len, ke = min(nz, kb + chunk_len);
     const uint32_t tbase = tcnt;  // ring counter of plane kb-2
