@@ -312,15 +312,19 @@ static nlse2shoc_status launch_stream(nlse2shoc_t H, Field &in, const CUtensorMa
   P.ncx = int((H->nx + C::TX - 1) / C::TX);
   P.ncy = DIMS == 3 ? int((H->ny + C::TY - 1) / C::TY) : 1;
   const int ncol = P.ncx * P.ncy;
-  // z-chunks: minimise rounds * (chunk length + priming cost)
-  int best = 1;
-  double bestc = 1e300;
+  // z-chunks: minimise rounds * (chunk length + priming cost).  3D: chunks of at most 64 planes
+  // where possible — neighbouring tiles of a round then stay close in z and their halo reads
+  // hit L2 (C4: 110-plane chunks 9.35 ms/step, 55-plane chunks 9.24).
+  int best = 1, best_any = 1;
+  double bestc = 1e300, bestc_any = 1e300;
   for (int nc = 1; nc <= 256 && 4 * nc <= H->nz + 3; ++nc) {
     const double rounds = std::ceil(double(ncol) * nc / G0);
     const double len = std::ceil(double(H->nz) / nc) + 1.5;
     const double c = rounds * len;
-    if (c < bestc - 1e-9) { bestc = c; best = nc; }
+    if (c < bestc_any - 1e-9) { bestc_any = c; best_any = nc; }
+    if ((DIMS != 3 || len - 1.5 <= 64.0) && c < bestc - 1e-9) { bestc = c; best = nc; }
   }
+  if (bestc > 1e299) best = best_any;
   static const int force_chunks = getenv("NLSE_NCHUNK") ? atoi(getenv("NLSE_NCHUNK")) : 0;
   if (force_chunks > 0) best = std::min<int>(force_chunks, int(H->nz));
   P.nchunk = best;
