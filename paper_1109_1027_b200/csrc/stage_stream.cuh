@@ -535,28 +535,34 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
           // interior point of this tile/plane reads.
           CT *s0 = tslot(k), *sm = tslot(k - 1), *spp = tslot(k + 1);
           auto at = [&](CT *s_, int lx, int ly) -> CT & { return s_[(ly + HY) * W + lx + 2]; };
-          if (zint) {
-            // x faces: rows of the tile (3D: interior rows only)
-            for (int task = ct; task < 2 * TY; task += C::NCW * 32) {
-              const bool hi = task >= TY;
-              if (hi ? !xhi : !xlo) continue;
-              const int ly = task % TY, gy = y0 + ly;
+          // Each ghost is formed by the warp that owns the depth-1 point reading it (x faces:
+          // the row's consumer thread; y faces: the consumer row's threads), so only a warp
+          // barrier is needed, not a CTA barrier.
+          auto owner = [&](int lx, int ly) { return ((ly / RPW) * CPT + lx / PPX) >> 5; };
+          // x faces: rows of the tile (3D: interior rows only)
+#pragma unroll
+          for (int hi = 0; hi < 2; ++hi) {
+            if (hi ? !xhi : !xlo) continue;
+            const int bx = hi ? nx - 1 : 0, lb = bx - x0, n = hi ? -1 : 1;
+            for (int ly = lane; ly < TY; ly += 32) {
+              const int gy = y0 + ly;
               if (DIMS == 3 && (gy < 1 || gy > ny - 2)) continue;
-              if (gy >= ny) continue;
-              const int bx = hi ? nx - 1 : 0, lb = bx - x0, n = hi ? -1 : 1;
+              if (gy >= ny || owner(lb + n, ly) != warp) continue;
               CT cbv = at(s0, lb, ly), cin = at(s0, lb + n, ly);
               CT D = lambda_b(P, cbv, potential(P, bx, gy, k));
               D = D - d2(at(sm, lb, ly), cbv, at(spp, lb, ly), P.ihz2);
               if (DIMS == 3) D = D - d2(at(s0, lb, ly - 1), cbv, at(s0, lb, ly + 1), P.ihy2);
               at(s0, lb - n, ly) = axpy(R(2) * cbv - cin, P.hx2, D);
             }
-            if (DIMS == 3) {
-              for (int task = ct; task < 2 * TX; task += C::NCW * 32) {
-                const bool hi = task >= TX;
-                if (hi ? !yhi : !ylo) continue;
-                const int lx = task % TX, gx = x0 + lx;
-                if (gx < 1 || gx > nx - 2) continue;
-                const int by = hi ? ny - 1 : 0, lb = by - y0, n = hi ? -1 : 1;
+          }
+          if (DIMS == 3) {
+#pragma unroll
+            for (int hi = 0; hi < 2; ++hi) {
+              if (hi ? !yhi : !ylo) continue;
+              const int by = hi ? ny - 1 : 0, lb = by - y0, n = hi ? -1 : 1;
+              for (int lx = lane; lx < TX; lx += 32) {
+                const int gx = x0 + lx;
+                if (gx < 1 || gx > nx - 2 || owner(lx, lb + n) != warp) continue;
                 CT cbv = at(s0, lx, lb), cin = at(s0, lx, lb + n);
                 CT D = lambda_b(P, cbv, potential(P, gx, by, k));
                 D = D - d2(at(sm, lx, lb), cbv, at(spp, lx, lb), P.ihz2);
@@ -566,7 +572,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
             }
           }
           fence_proxy_async_smem();  // generic writes to slots precede later TMA refills
-          named_bar_sync(1, C::NCW * 32);
+          __syncwarp();
         }
       }
       // streamed-axis faces: the ghost plane -1 (read as plane k-2 at k = 1) and the ghost
