@@ -441,6 +441,8 @@ template <typename R, int MODE>
 static nlse2shoc_status launch_line(nlse2shoc_t H, const void *in, const void *psi, const void *acc, StageParams<R> P,
                                     cudaStream_t st) {
   const int threads = 256;
+  static const bool no_rev = getenv("NLSE_NO_REV") != nullptr;
+  P.rev = (!no_rev && (MODE == M_S2 || MODE == M_S4 || MODE == M_S2R || MODE == M_S4R)) ? 1 : 0;
   // complex128: the grid-stride kernel (L1 serves the stencil overlap) measured faster than the
   // shared-memory tiles on C2 (0.197 vs 0.214 ms/step); complex64: tiles (0.125 vs 0.134)
   if (sizeof(R) == 8) {

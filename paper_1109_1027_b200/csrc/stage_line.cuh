@@ -71,7 +71,8 @@ __global__ void __launch_bounds__(256) stage_line_kernel(const cplx<R> *__restri
                                                          const cplx<R> *__restrict__ acc, const StageParams<R> P) {
   using CT = cplx<R>;
   const int n = P.nx;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+  for (int64_t i0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i0 < n; i0 += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = P.rev ? n - 1 - i0 : i0;  // reversed: start on what the last stage wrote last
     CT c, L;
     const CT t = line_point(Tin, i, n, P, c, L);
     if (MODE == M_LAP) {
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(256) line_tile_kernel(const cplx<R> *__restric
   constexpr int TILE = 256 * PT;
   __shared__ __align__(16) CT sT[TILE + 8];  // sT[k] = Tin[t0 - 4 + k]
   const int n = P.nx;
-  const int64_t t0 = int64_t(blockIdx.x) * TILE;
+  const int64_t t0 = int64_t(P.rev ? gridDim.x - 1 - blockIdx.x : blockIdx.x) * TILE;
   for (int k = threadIdx.x; k < TILE + 8; k += 256) {
     const int64_t g = t0 - 4 + k;
     sT[k] = (g >= 0 && g < n) ? Tin[g] : mk<R>(R(0), R(0));
