@@ -71,3 +71,17 @@ def test_product_package_never_imports_oracle():
                 code = re.sub(r'"""(.|\n)*?"""', "", code)
                 assert "oracle" not in code.lower(), f
                 assert "icgen" not in code, f
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No fallback: with the shared library absent, the first call raises ImportError naming
+    the missing file (checked in a fresh interpreter)."""
+    import subprocess
+    import sys
+
+    missing = tmp_path / "libnlse2shoc.so"
+    code = ("import paper_1109_1027_b200 as nl\n"
+            "try:\n    nl.nlse2shoc_version()\nexcept ImportError as e:\n    print('IMPORTERROR', e)\n")
+    env = dict(os.environ, NLSE_LIB=str(missing))
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=120)
+    assert "IMPORTERROR" in r.stdout and str(missing) in r.stdout, r.stdout + r.stderr
