@@ -537,7 +537,7 @@ static nlse2shoc_status launch_stage(nlse2shoc_t H, Field &psi, int s, double dt
   Field &in = stage_input(H, psi, s);
   cplx<R> *pPsi = reinterpret_cast<cplx<R> *>(psi.ptr), *pA = reinterpret_cast<cplx<R> *>(H->TA.ptr),
           *pB = reinterpret_cast<cplx<R> *>(H->TB.ptr), *pAcc = reinterpret_cast<cplx<R> *>(H->acc.ptr);
-  // reconstructed-accumulator form (14 transfers per point-step): fused variant 0
+  // reconstructed-accumulator form (13 transfers per point-step): variant 0
   const bool recon = H->variant == 0;
   switch (s) {
     case 1:

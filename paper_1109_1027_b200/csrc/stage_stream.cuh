@@ -8,12 +8,13 @@
 //     ghost = h_d^2 D_d(b) + 2 Psi_b - Psi_{b+n}, D_d(b) = lambda_b - sum_{e!=d} delta_e^2 Psi_b,
 //     computed in shared memory by the CTA that needs it (no extra pass, no padded arrays);
 //   * F = i(a Lap + (s|Psi|^2 - V) Psi) with the Psi_t boundary rule;
-//   * the RK4 stage combine in Psi-space accumulator form (16 field
-//     transfers per point-step instead of the listing's 17).
+//   * the RK4 stage combine in Psi-space accumulator form: 13 field transfers
+//     per point-step with the reconstructed accumulator (default), 16 with the explicit one;
+//     the paper's listing costs 17.
 //
 // Data movement: the slowest axis ("z"; y in 2D) is streamed.  A producer warp issues TMA
 // boxes of one plane (tile + 2-cell halo) into a ring of shared-memory slots guarded by
-// mbarriers, and the Psi^n / acc tiles the stage needs into a second ring; 8 consumer warps
+// mbarriers, and the Psi^n / acc tiles the stage needs into a second ring; the consumer warps
 // compute plane k from slots k-2..k+2 and store T_s / acc with 128-bit stores.  Work is
 // split into (column, z-chunk) tiles assigned round-robin to a persistent grid so that
 // concurrently running CTAs work on neighbouring columns at the same z (halo re-reads hit
