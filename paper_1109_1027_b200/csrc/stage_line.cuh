@@ -206,36 +206,56 @@ __global__ void __launch_bounds__(1024, 1) resident_line_kernel(cplx<R> *__restr
 template <typename R>
 __global__ void __launch_bounds__(256) reduce_N_kernel(const cplx<R> *__restrict__ psi, const StageParams<R> P,
                                                        double *__restrict__ part) {
-  double lo = INFINITY, hi = -INFINITY, bad = 0;
+  // Each warp scans one contiguous range of the (caller-layout, pitch == nx) field, lanes
+  // interleaved for coalescing; the (x, y, z) index of its lane advances by 32 per iteration
+  // with carries instead of a division per element.
+  R lo = R(INFINITY), hi = R(-INFINITY);
+  double bad = 0;
   const int64_t total = int64_t(P.nx) * P.ny * P.nz;
-  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < total; q += int64_t(gridDim.x) * blockDim.x) {
-    const int gx = int(q % P.nx);
-    const int64_t r = q / P.nx;
-    const int gy = int(r % P.ny), lz = int(r / P.ny);
-    const cplx<R> c = psi[(int64_t(lz) * P.ny + gy) * P.pitch + gx];
-    if (!isfinite(c.re) || !isfinite(c.im)) bad += 1;
-    const double N = double(fma(P.s, norm2(c), -potential(P, gx, gy, lz)));
-    lo = fmin(lo, N);
-    hi = fmax(hi, N);
+  const int64_t nwarps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  const int64_t wid = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t chunk = ((total + nwarps - 1) / nwarps + 31) & ~int64_t(31);
+  const int64_t q0 = wid * chunk + (threadIdx.x & 31), q1 = min(total, (wid + 1) * chunk);
+  if (q0 < q1) {
+    int gx = int(q0 % P.nx);
+    int64_t r = q0 / P.nx;
+    int gy = int(r % P.ny), lz = int(r / P.ny);
+    for (int64_t q = q0; q < q1; q += 32) {
+      const cplx<R> c = psi[q];
+      if (!isfinite(c.re) || !isfinite(c.im)) bad += 1;
+      const R N = fma(P.s, norm2(c), -potential(P, gx, gy, lz));
+      lo = fmin(lo, N);
+      hi = fmax(hi, N);
+      gx += 32;
+      while (gx >= P.nx) {
+        gx -= P.nx;
+        if (++gy == P.ny) {
+          gy = 0;
+          ++lz;
+        }
+      }
+    }
   }
   for (int o = 16; o > 0; o >>= 1) {
     lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
     hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
     bad += __shfl_xor_sync(0xffffffffu, bad, o);
   }
-  __shared__ double s[3][8];
+  __shared__ R s[2][8];
+  __shared__ double sb[8];
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) { s[0][w] = lo; s[1][w] = hi; s[2][w] = bad; }
+  if (l == 0) { s[0][w] = lo; s[1][w] = hi; sb[w] = bad; }
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int i = 1; i < int(blockDim.x >> 5); ++i) {
       lo = fmin(lo, s[0][i]);
       hi = fmax(hi, s[1][i]);
-      bad += s[2][i];
+      bad += sb[i];
     }
-    part[3 * blockIdx.x] = lo;
-    part[3 * blockIdx.x + 1] = hi;
-    part[3 * blockIdx.x + 2] = bad;
+    const int b = blockIdx.x;
+    part[3 * b] = double(lo);
+    part[3 * b + 1] = double(hi);
+    part[3 * b + 2] = bad;
   }
 }
 
