@@ -444,14 +444,21 @@ static nlse2shoc_status launch_line(nlse2shoc_t H, const void *in, const void *p
   static const bool no_rev = getenv("NLSE_NO_REV") != nullptr;
   P.rev = (!no_rev && (MODE == M_S2 || MODE == M_S4 || MODE == M_S2R || MODE == M_S4R)) ? 1 : 0;
   // complex128: the grid-stride kernel (L1 serves the stencil overlap) measured faster than the
-  // shared-memory tiles on C2 (0.197 vs 0.214 ms/step); complex64: tiles (0.125 vs 0.134)
-  if (sizeof(R) == 8) {
+  // shared-memory tiles on C2 (0.191 vs 0.205-0.230 ms/step); complex64: tiles of 256 points
+  // (C2 0.110 ms; 512 / 1024 / 2048-point tiles 0.128 / 0.119 / 0.115, grid-stride 0.125)
+#ifndef NLSE_LINE_TILE_C128
+#define NLSE_LINE_TILE_C128 0
+#endif
+#ifndef NLSE_LINE_PT
+#define NLSE_LINE_PT 1
+#endif
+  if (sizeof(R) == 8 && !NLSE_LINE_TILE_C128) {
     const int64_t blocks = std::min<int64_t>((H->nx + threads - 1) / threads, int64_t(H->num_sms) * 8);
     stage_line_kernel<R, MODE><<<int(blocks), threads, 0, st>>>(
         reinterpret_cast<const cplx<R> *>(in), reinterpret_cast<const cplx<R> *>(psi),
         reinterpret_cast<const cplx<R> *>(acc), P);
   } else {
-    constexpr int PT = 4;
+    constexpr int PT = NLSE_LINE_PT;
     const int64_t blocks = (H->nx + threads * PT - 1) / (threads * PT);
     line_tile_kernel<R, MODE, PT><<<int(blocks), threads, 0, st>>>(
         reinterpret_cast<const cplx<R> *>(in), reinterpret_cast<const cplx<R> *>(psi),
