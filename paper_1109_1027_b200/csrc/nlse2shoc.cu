@@ -82,6 +82,10 @@ struct nlse2shoc_s {
   nlse2shoc_potential V{};
   int bc = 0, dtype = 0, device = 0, variant = 0, scheme = 0;
   int D_fields = 0;  // D fields allocated for the two-kernel variants
+  int rng_b = 0, rng_e = 0;  // plane range of the next stage launch (0, 0: the whole slab)
+  int reserve_sms = 0;       // SMs left free for a concurrent NCCL exchange (interior launches)
+  cudaStream_t comm_st = nullptr;  // edge-first halo exchange: side stream + events
+  cudaEvent_t ev_edge = nullptr, ev_recv = nullptr;
   nlse2shoc_alloc_fn alloc = nullptr;  // device allocator captured at create (null: cudaMalloc)
   nlse2shoc_free_fn dfree = nullptr;
   void *alloc_ctx = nullptr;
@@ -236,6 +240,8 @@ template <typename R> static void fill_params(nlse2shoc_t H, StageParams<R> &P) 
   P.nx = int(H->nx);
   P.ny = int(H->ny);
   P.nz = int(H->nz);
+  P.zb = H->rng_e > 0 ? H->rng_b : 0;  // plane range of this launch (edge / interior split)
+  P.ze = H->rng_e > 0 ? H->rng_e : int(H->nz);
   P.z0 = int(H->z0);
   P.NZ = int(H->NZ);
   P.lo_face = H->z0 == 0;
@@ -308,7 +314,7 @@ static nlse2shoc_status launch_stream(nlse2shoc_t H, Field &in, const CUtensorMa
   int occ = 1;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stage_stream_kernel<DIMS, R, MODE>, LY::NTHREADS, smem));
   occ = std::max(occ, 1);
-  const int G0 = H->num_sms * occ;
+  const int G0 = std::max(1, H->num_sms - H->reserve_sms) * occ;
   P.ncx = int((H->nx + C::TX - 1) / C::TX);
   P.ncy = DIMS == 3 ? int((H->ny + C::TY - 1) / C::TY) : 1;
   const int ncol = P.ncx * P.ncy;
@@ -317,16 +323,17 @@ static nlse2shoc_status launch_stream(nlse2shoc_t H, Field &in, const CUtensorMa
   // hit L2 (C4: 110-plane chunks 9.35 ms/step, 55-plane chunks 9.24).
   int best = 1, best_any = 1;
   double bestc = 1e300, bestc_any = 1e300;
-  for (int nc = 1; nc <= 256 && 4 * nc <= H->nz + 3; ++nc) {
+  const int nzr = P.ze - P.zb;  // planes this launch computes
+  for (int nc = 1; nc <= 256 && 4 * nc <= nzr + 3; ++nc) {
     const double rounds = std::ceil(double(ncol) * nc / G0);
-    const double len = std::ceil(double(H->nz) / nc) + 1.5;
+    const double len = std::ceil(double(nzr) / nc) + 1.5;
     const double c = rounds * len;
     if (c < bestc_any - 1e-9) { bestc_any = c; best_any = nc; }
     if ((DIMS != 3 || len - 1.5 <= 64.0) && c < bestc - 1e-9) { bestc = c; best = nc; }
   }
   if (bestc > 1e299) best = best_any;
   static const int force_chunks = getenv("NLSE_NCHUNK") ? atoi(getenv("NLSE_NCHUNK")) : 0;
-  if (force_chunks > 0) best = std::min<int>(force_chunks, int(H->nz));
+  if (force_chunks > 0) best = std::min<int>(force_chunks, nzr);
   P.nchunk = best;
   P.ntiles = ncol * best;
   const int G = std::min(G0, P.ntiles);
@@ -646,6 +653,63 @@ static bool resident_ok(nlse2shoc_t H) {
          size_t(4) * size_t(H->nx) * H->S <= size_t(200) * 1024 && !getenv("NLSE_NO_RESIDENT");
 }
 
+// Edge-first halo exchange: per stage, the 2 edge planes at each slab end
+// (the ones that read halos and that the neighbours need) are computed first, their exchange
+// runs on a side stream while the interior planes are computed, and the next stage's edges
+// wait for it.  Fused 2D/3D variants (0, 2) on slabs of >= 8 planes; NLSE_NO_OVERLAP=1 off.
+static bool overlap_ok(const View &v) {
+  static const bool off = getenv("NLSE_NO_OVERLAP") != nullptr;
+  if (off) return false;
+  bool multi = v.hs.size() > 1;
+  for (nlse2shoc_t H : v.hs) {
+    if (H->dims < 2 || (H->variant != 0 && H->variant != 2) || H->nz < 8) return false;
+    multi = multi || (H->sharded && H->nranks > 1);
+  }
+  return multi;
+}
+
+static nlse2shoc_status stage_range(nlse2shoc_t H, Field &psi, int s, double dt, int zb, int ze, cudaStream_t st) {
+  H->rng_b = zb;
+  H->rng_e = ze;
+  const nlse2shoc_status r = stage(H, psi, s, dt, nullptr, st);
+  H->rng_b = H->rng_e = 0;
+  return r;
+}
+
+static nlse2shoc_status run_rk4_overlapped(View &v, double dt, int64_t nsteps, cudaStream_t st) {
+  nlse2shoc_t H0 = v.hs[0];
+  if (!H0->comm_st) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&H0->comm_st, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&H0->ev_edge, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&H0->ev_recv, cudaEventDisableTiming));
+  }
+  cudaStream_t cs = H0->comm_st;
+  TRY(exchange(v, 1, st));  // Psi's halos for the first stage
+  for (int64_t n = 0; n < nsteps; ++n)
+    for (int s = 1; s <= 4; ++s) {
+      for (size_t i = 0; i < v.hs.size(); ++i) {
+        const int nz = int(v.hs[i]->nz);
+        TRY(stage_range(v.hs[i], v.psis[i], s, dt, 0, 2, st));
+        TRY(stage_range(v.hs[i], v.psis[i], s, dt, nz - 2, nz, st));
+      }
+      // stage s's output is stage s+1's input (s = 4: Psi, the next step's stage 1 input)
+      CUDA_TRY(cudaEventRecord(H0->ev_edge, st));
+      CUDA_TRY(cudaStreamWaitEvent(cs, H0->ev_edge, 0));
+      TRY(exchange(v, s == 4 ? 1 : s + 1, cs));
+      CUDA_TRY(cudaEventRecord(H0->ev_recv, cs));
+      for (size_t i = 0; i < v.hs.size(); ++i) {
+        // a real NCCL exchange runs kernels: leave it a few SMs beside the persistent grid
+        nlse2shoc_t H = v.hs[i];
+        H->reserve_sms = (H->sharded && H->nranks > 1) ? 8 : 0;
+        const nlse2shoc_status r = stage_range(H, v.psis[i], s, dt, 2, int(H->nz) - 2, st);
+        H->reserve_sms = 0;
+        TRY(r);
+      }
+      CUDA_TRY(cudaStreamWaitEvent(st, H0->ev_recv, 0));
+    }
+  return NLSE2SHOC_OK;
+}
+
 static nlse2shoc_status run_rk4(View &v, double dt, int64_t nsteps, cudaStream_t st) {
   if (v.hs.size() == 1 && v.hs[0]->variant == 4) return rk4_pairs(v.hs[0], v.psis[0], dt, nsteps, st);
   if (v.hs.size() == 1 && resident_ok(v.hs[0])) {
@@ -653,6 +717,7 @@ static nlse2shoc_status run_rk4(View &v, double dt, int64_t nsteps, cudaStream_t
     return H->dtype == NLSE2SHOC_C64 ? rk4_resident_1d<float>(H, v.psis[0], dt, nsteps, st)
                                      : rk4_resident_1d<double>(H, v.psis[0], dt, nsteps, st);
   }
+  if (overlap_ok(v)) return run_rk4_overlapped(v, dt, nsteps, st);
   for (int64_t n = 0; n < nsteps; ++n)
     for (int s = 1; s <= 4; ++s) {
       TRY(exchange(v, s, st));
@@ -1203,6 +1268,9 @@ void nlse2shoc_destroy(nlse2shoc_t H) {
   if (H->prog) dev_free(H, H->prog);
   if (H->rbar) dev_free(H, H->rbar);
   if (H->red) dev_free(H, H->red);
+  if (H->ev_edge) cudaEventDestroy(H->ev_edge);
+  if (H->ev_recv) cudaEventDestroy(H->ev_recv);
+  if (H->comm_st) cudaStreamDestroy(H->comm_st);
 #ifdef NLSE_WITH_NCCL
   if (H->comm) ncclCommDestroy(H->comm);
 #endif

@@ -180,6 +180,7 @@ template <typename R> struct StageParams {
   R ca, cb;              // stage-combine coefficients (acc, T)
   R cA;                  // phase-A coefficient of the stage-pair kernel (stage_pair.cuh)
   int rev;               // traverse the tiles in reverse order (alternate stages: L2 reuse)
+  int zb, ze;            // local planes [zb, ze) this launch computes (edge / interior split)
   int bc;                // 0 Dirichlet, 1 Laplacian-zero, 2 MSD (1D line kernels only)
   int vkind;             // 0 none, 1 harmonic tables, 2 array
   const R *vx, *vy, *vz; // harmonic tables (vz indexed by GLOBAL streamed index)
@@ -322,7 +323,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
   __syncthreads();
 
   const int G = gridDim.x;
-  const int chunk_len = (P.nz + P.nchunk - 1) / P.nchunk;
+  const int chunk_len = (P.ze - P.zb + P.nchunk - 1) / P.nchunk;
   const int ncol = P.ncx * P.ncy;
 
   if (warp == C::NCW) {
@@ -350,7 +351,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
         const int tt = P.rev ? P.ntiles - 1 - t : t;  // reversed order: read the L2-resident tail first
         const int chunk = tt / ncol, col = tt % ncol;
         const int x0 = (col % P.ncx) * TX, y0 = (col / P.ncx) * TY;
-        const int kb = chunk * chunk_len, ke = min(P.nz, kb + chunk_len);
+        const int kb = P.zb + chunk * chunk_len, ke = min(P.ze, kb + chunk_len);
         // Round barrier: every producer starts round r only after all producers finished
         // issuing round r-1, so the tiles of a round stream the same planes at the same time
         // and a tile's halo rows/columns are L2 hits when its neighbours load them.
@@ -467,7 +468,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
     const int tt = P.rev ? P.ntiles - 1 - t : t;
     const int chunk = tt / ncol, col = tt % ncol;
     const int x0 = (col % P.ncx) * TX, y0 = (col / P.ncx) * TY;
-    const int kb = chunk * chunk_len, ke = min(nz, kb + chunk_len);
+    const int kb = P.zb + chunk * chunk_len, ke = min(P.ze, kb + chunk_len);
     const uint32_t tbase = tcnt;  // ring counter of plane kb-2
     auto tslot = [&](int p) -> CT * { return ring + size_t((tbase + uint32_t(p - kb + 2)) % RT) * LY::SLOT; };
     auto twait = [&](int p) {
