@@ -186,6 +186,19 @@ __device__ __forceinline__ void st_stream(float4 *p, float4 v) { *p = v; }
 __device__ __forceinline__ void st_stream(double2 *p, double2 v) { *p = v; }
 #endif
 
+// accumulator stores (NLSE_ACC_STORE=1: evict-first, since acc is re-read only two stages
+// later; measured no better than plain stores on C4 / C5W, so plain is the default)
+#ifndef NLSE_ACC_STORE
+#define NLSE_ACC_STORE 0
+#endif
+#if NLSE_ACC_STORE == 1
+__device__ __forceinline__ void st_acc(float4 *p, float4 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_acc(double2 *p, double2 v) { __stcs(p, v); }
+#else
+__device__ __forceinline__ void st_acc(float4 *p, float4 v) { *p = v; }
+__device__ __forceinline__ void st_acc(double2 *p, double2 v) { *p = v; }
+#endif
+
 __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t *p) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

@@ -346,6 +346,10 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
 #endif
       const uint64_t pol_keep = NLSE_TPOL == 2 ? policy_evict_last() : (NLSE_TPOL == 1 ? policy_evict_normal() : policy_evict_first());
       const uint64_t pol_stream = NLSE_PPOL == 0 ? policy_evict_first() : policy_evict_normal();
+#ifndef NLSE_ACC_LOAD_FIRST
+#define NLSE_ACC_LOAD_FIRST 0
+#endif
+      const uint64_t pol_acc = NLSE_ACC_LOAD_FIRST ? policy_evict_first() : pol_stream;
       uint32_t tcnt = 0, pcnt = 0;
       for (int t = blockIdx.x; t < P.ntiles; t += G) {
         const int tt = P.rev ? P.ntiles - 1 - t : t;  // reversed order: read the L2-resident tail first
@@ -429,8 +433,10 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
             for (int b = 0; b < C::NBOXP; ++b) {
               const int c0 = x0 * LY::EPC + b * LY::BWP;
               char *d = reinterpret_cast<char *>(dst + (q == 0 ? 0 : ACC_OFF)) + b * LY::BWP * 8;
-              if (DIMS == 3) tma_load_3d_hint(d, m, &fullP[slot], c0, y0, k, pol_stream);
-              else tma_load_2d_hint(d, m, &fullP[slot], c0, k, pol_stream);
+              // Psi^n is re-read by the next stage (L2 reuse); acc is not
+              const uint64_t pol = q == 0 ? pol_stream : pol_acc;
+              if (DIMS == 3) tma_load_3d_hint(d, m, &fullP[slot], c0, y0, k, pol);
+              else tma_load_2d_hint(d, m, &fullP[slot], c0, k, pol);
             }
           }
           ++pcnt;
@@ -700,7 +706,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
 #pragma unroll
           for (int v = 0; v < PPX / VV::CPV; ++v) {
             st_stream(reinterpret_cast<typename VV::T *>(oTr) + v, VV::join(oT + v * VV::CPV));
-            if (LY::template writes_acc<MODE>()) st_stream(reinterpret_cast<typename VV::T *>(oAr) + v, VV::join(oA + v * VV::CPV));
+            if (LY::template writes_acc<MODE>()) st_acc(reinterpret_cast<typename VV::T *>(oAr) + v, VV::join(oA + v * VV::CPV));
           }
         } else {
 #pragma unroll
@@ -819,7 +825,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
         for (int v = 0; v < PPX / VV::CPV; ++v) {
           st_stream(reinterpret_cast<typename VV::T *>(outT + r * pitch) + v, VV::join(oT + v * VV::CPV));
           if (LY::template writes_acc<MODE>())
-            st_stream(reinterpret_cast<typename VV::T *>(outA + r * pitch) + v, VV::join(oA + v * VV::CPV));
+            st_acc(reinterpret_cast<typename VV::T *>(outA + r * pitch) + v, VV::join(oA + v * VV::CPV));
         }
 #pragma unroll
         for (int q = 0; q < PPX; ++q) {
