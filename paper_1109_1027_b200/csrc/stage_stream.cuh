@@ -81,8 +81,16 @@ template <> struct Cfg<3, float> : Rings<68 * (NLSE3F_TY + 4) * 8, 64 * NLSE3F_T
   static constexpr int TX = 64, TY = NLSE3F_TY, PPX = 2, RPW = NLSE3F_RPW, NCW = NLSE3F_NCW, NBOX = 1, NBOXP = 1,
                        W = 68;
 };
-template <> struct Cfg<3, double> : Rings<36 * (28 + 4) * 16, 32 * 28 * 16> {
-  static constexpr int TX = 32, TY = 28, PPX = 1, RPW = 2, NCW = 14, NBOX = 1, NBOXP = 1, W = 36;
+// 3D complex128 tiles: 32 x 32, 8 consumer warps x 4 rows (sweep on C5W c128, ms/step:
+// 32x28/14 warps x 2 rows 4.38, 32x32/8x4 4.24, 32x40/10x4 4.25, 32x20/10x2 4.29, 32x24/12x2 4.32)
+#ifndef NLSE3D_TY
+#define NLSE3D_TY 32
+#define NLSE3D_NCW 8
+#define NLSE3D_RPW 4
+#endif
+template <> struct Cfg<3, double> : Rings<36 * (NLSE3D_TY + 4) * 16, 32 * NLSE3D_TY * 16> {
+  static constexpr int TX = 32, TY = NLSE3D_TY, PPX = 1, RPW = NLSE3D_RPW, NCW = NLSE3D_NCW, NBOX = 1, NBOXP = 1,
+                       W = 36;
 };
 // 2D: the streamed axis is y and a "plane" is one row of TX + halo (slots split into
 // 128-byte-aligned TMA boxes of <= 256 eight-byte elements).  Presets (NLSE2D_PRESET, for
