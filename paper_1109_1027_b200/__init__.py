@@ -153,21 +153,37 @@ class Solver:
         code = {"2shoc": 0, "cd": 1}.get(scheme, scheme)
         check(lib().nlse2shoc_set_scheme(self._h, int(code)), "set_scheme")
 
+    def _check(self, t, name="psi"):
+        """The C ABI takes raw pointers: check what it cannot (device, dtype, layout, shape)."""
+        import torch
+
+        want = torch.complex64 if self.dtype == "c64" else torch.complex128
+        if not isinstance(t, torch.Tensor) or not t.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor")
+        if t.dtype != want:
+            raise ValueError(f"{name} has dtype {t.dtype}, the handle computes in {want}")
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous ([z][y][x], x fastest)")
+        if tuple(t.shape) != tuple(self.local_shape):
+            raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(self.local_shape)}")
+        return t
+
     def laplacian(self, psi, out=None, stream=None):
         import torch
 
+        self._check(psi)
         if out is None:
             out = torch.empty_like(psi)
-        return nlse2shoc_laplacian(self._h, psi, out, stream)
+        return nlse2shoc_laplacian(self._h, psi, self._check(out, "out"), stream)
 
     def rk4(self, psi, dt, nsteps, stream=None):
-        return nlse2shoc_rk4(self._h, psi, dt, nsteps, stream)
+        return nlse2shoc_rk4(self._h, self._check(psi), dt, nsteps, stream)
 
     def stability_bound(self, psi, stream=None) -> float:
-        return nlse2shoc_stability_bound(self._h, psi, stream)
+        return nlse2shoc_stability_bound(self._h, self._check(psi), stream)
 
     def check_finite(self, psi, stream=None):
-        nlse2shoc_check_finite(self._h, psi, stream)
+        nlse2shoc_check_finite(self._h, self._check(psi), stream)
 
     @property
     def workspace_bytes(self) -> int:

@@ -222,3 +222,15 @@ def test_workspace_comes_from_torch_allocator():
     S.close()
     torch.cuda.synchronize()
     assert torch.cuda.memory_allocated() <= before + g.numel() * 8 + 512  # allocator rounding
+
+
+def test_binding_rejects_mismatched_tensors():
+    """The C ABI takes raw pointers; the binding checks device, dtype, layout and shape."""
+    w = configs.SMALL(3, (21, 17, 9), "dirichlet", "c64")
+    S = H.gpu_solver(w, "c64")
+    good = _dev(H.psi0_host(w, "c64"))
+    bad = [good.to(torch.complex128), good.cpu(), good.transpose(0, 2), good[:, :, :-1].contiguous()]
+    for t in bad:
+        with pytest.raises(ValueError):
+            S.rk4(t, 1e-4, 1)
+    S.rk4(good, 1e-4, 1)
