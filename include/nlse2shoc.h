@@ -81,7 +81,8 @@ typedef struct {
   const void *data;
 } nlse2shoc_potential;
 
-/* Create a single-GPU handle on the current CUDA device.
+/* Create a single-GPU handle on the current CUDA device.  Every later call on the handle runs
+ * on that device whatever device is current, and restores the caller's current device.
  *  out   : receives the handle (host pointer).
  *  dims  : 1, 2 or 3.          N : counts (x, y, z), N[d] >= 5 for d < dims, 1 otherwise.
  *  h     : spacing per axis, finite and > 0 (anisotropic allowed; R17).

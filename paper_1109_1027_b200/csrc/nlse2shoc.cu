@@ -6,6 +6,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -294,12 +295,26 @@ template <typename R> static void fill_params(nlse2shoc_t H, StageParams<R> &P) 
 }
 
 // ------------------------------------------------------------------------ launch plans
+// Kernel attributes are per device: remember, per kernel instantiation, which devices have
+// been configured (a process may drive several GPUs).
+static bool attr_needed(std::atomic<uint64_t> &mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = uint64_t(1) << (dev & 63);
+  return (mask.load(std::memory_order_relaxed) & bit) == 0;
+}
+static void attr_done(std::atomic<uint64_t> &mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  mask.fetch_or(uint64_t(1) << (dev & 63), std::memory_order_relaxed);
+}
+
 template <int DIMS, typename R, int MODE> static nlse2shoc_status set_smem_attr() {
-  static bool done = false;
-  if (!done) {
+  static std::atomic<uint64_t> done{0};
+  if (attr_needed(done)) {
     CUDA_TRY(cudaFuncSetAttribute(stage_stream_kernel<DIMS, R, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(Layout<DIMS, R>::template smem_bytes<MODE>())));
-    done = true;
+    attr_done(done);
   }
   return NLSE2SHOC_OK;
 }
@@ -380,11 +395,11 @@ static nlse2shoc_status launch_pair(nlse2shoc_t H, const CUtensorMap &tin, const
   using C = PCfg<DIMS, R>;
   using LY = PLayout<DIMS, R>;
   const size_t smem = LY::template smem_bytes<PAIR>();
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (attr_needed(attr)) {
     CUDA_TRY(cudaFuncSetAttribute(pair_stream_kernel<DIMS, R, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(smem)));
-    attr = true;
+    attr_done(attr);
   }
   int occ = 1;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pair_stream_kernel<DIMS, R, PAIR>, LY::NTHREADS, smem));
@@ -633,11 +648,11 @@ template <typename R> static nlse2shoc_status rk4_resident_1d(nlse2shoc_t H, Fie
   StageParams<R> P;
   fill_params<R>(H, P);
   const size_t smem = size_t(4) * size_t(H->nx) * sizeof(cplx<R>);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (attr_needed(attr)) {
     CUDA_TRY(cudaFuncSetAttribute(resident_line_kernel<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CUDA_TRY(cudaFuncSetAttribute(resident_line_kernel<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
+    attr_done(attr);
   }
   if (H->bc == NLSE2SHOC_BC_MSD)
     resident_line_kernel<R, true><<<1, 1024, smem, st>>>(reinterpret_cast<cplx<R> *>(psi.ptr), nsteps, R(dt), P);
@@ -997,6 +1012,18 @@ static void reset_launches(nlse2shoc_t H) {
   for (nlse2shoc_t S : H->slabs) S->launches = 0;
 }
 
+// Every call runs on the handle's device and restores the caller's current device.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 static nlse2shoc_status check_ptr(const void *p, const char *name) {
   if (!p) return fail(NLSE2SHOC_EINVAL, std::string(name) + " is NULL");
   if (reinterpret_cast<uintptr_t>(p) % 16) return fail(NLSE2SHOC_EINVAL, std::string(name) + " is not 16-byte aligned");
@@ -1129,6 +1156,7 @@ size_t nlse2shoc_workspace_bytes(nlse2shoc_t H) {
 
 nlse2shoc_status nlse2shoc_set_variant(nlse2shoc_t H, int variant) {
   if (!H) return fail(NLSE2SHOC_EINVAL, "NULL handle");
+  DeviceGuard dg(H->device);
   if (variant < 0 || variant > 4)
     return fail(NLSE2SHOC_EINVAL, "variant must be 0 (fused), 1 (two-kernel), 2 (fused, 16-transfer "
                                   "accumulator), 3 (two-kernel, multi-storage) or 4 (stage pairs)");
@@ -1155,6 +1183,7 @@ nlse2shoc_status nlse2shoc_set_scheme(nlse2shoc_t H, int scheme) {
 
 nlse2shoc_status nlse2shoc_laplacian(nlse2shoc_t H, const void *psi, void *L, void *stream) {
   if (!H) return fail(NLSE2SHOC_EINVAL, "NULL handle");
+  DeviceGuard dg(H->device);
   TRY(check_ptr(psi, "psi"));
   TRY(check_ptr(L, "L"));
   if (psi == L) return fail(NLSE2SHOC_EINVAL, "psi and L must be distinct");
@@ -1177,6 +1206,7 @@ nlse2shoc_status nlse2shoc_laplacian(nlse2shoc_t H, const void *psi, void *L, vo
 
 nlse2shoc_status nlse2shoc_rk4(nlse2shoc_t H, void *psi, double dt, int64_t nsteps, void *stream) {
   if (!H) return fail(NLSE2SHOC_EINVAL, "NULL handle");
+  DeviceGuard dg(H->device);
   TRY(check_ptr(psi, "psi"));
   if (!finite_pos(dt)) return fail(NLSE2SHOC_EINVAL, "dt must be finite and > 0");
   if (nsteps < 0) return fail(NLSE2SHOC_EINVAL, "nsteps must be >= 0");
@@ -1192,6 +1222,7 @@ nlse2shoc_status nlse2shoc_rk4(nlse2shoc_t H, void *psi, double dt, int64_t nste
 
 nlse2shoc_status nlse2shoc_stability_bound(nlse2shoc_t H, const void *psi, double *kmax, void *stream) {
   if (!H || !kmax) return fail(NLSE2SHOC_EINVAL, "NULL argument");
+  DeviceGuard dg(H->device);
   TRY(check_ptr(psi, "psi"));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   double r[3];
@@ -1214,6 +1245,7 @@ nlse2shoc_status nlse2shoc_stability_bound(nlse2shoc_t H, const void *psi, doubl
 
 nlse2shoc_status nlse2shoc_check_finite(nlse2shoc_t H, const void *psi, void *stream) {
   if (!H) return fail(NLSE2SHOC_EINVAL, "NULL handle");
+  DeviceGuard dg(H->device);
   TRY(check_ptr(psi, "psi"));
   double r[3];
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -1256,6 +1288,7 @@ const char *nlse2shoc_version(void) {
 
 void nlse2shoc_destroy(nlse2shoc_t H) {
   if (!H) return;
+  DeviceGuard dg(H->device);
   cudaDeviceSynchronize();
   for (nlse2shoc_t S : H->slabs) nlse2shoc_destroy(S);
   if (H->Lw) dev_free(H, H->Lw);
