@@ -156,15 +156,39 @@ def parse(csv_path, order_path):
         print(json.dumps(r))
 
 
+def report(time_path, ncu_path, peaks_path):
+    """Markdown table from the timing JSON lines and the parsed ncu JSON lines."""
+    T = [json.loads(l) for l in open(time_path)]
+    Nc = {(r["dims"], r["row"]): r for r in map(json.loads, open(ncu_path))}
+    pk = json.load(open(peaks_path))["hbm_gbs"]
+    out = ["| dims | workload | realisation | storage (N) | Laplacian ms | RK4 step ms | pt-steps/s | DRAM B/pt Lap | "
+           "DRAM B/pt step | step GB/s (DRAM) | frac of HBM |", "|---|---|---|---|---|---|---|---|---|---|---|"]
+    for r in T:
+        n = Nc[(r["dims"], r["row"])]
+        gbs = n["step_dram_B_per_pt"] * r["npts"] / (r["step_ms"] * 1e-3) / 1e9
+        out.append(f"| {r['dims']} | {r['workload']} | {r['row']} | {r['storage_N']} | {r['lap_ms']:.3f} | "
+                   f"{r['step_ms']:.3f} | {r['pt_steps_per_s']:.3e} | {n['lap_dram_B_per_pt']:.1f} | "
+                   f"{n['step_dram_B_per_pt']:.1f} | {gbs:.0f} | {gbs / pk:.2f} |")
+    out += ["", "Paper's static counts (Tables 3-5): Laplacian ops / storage, RK4 ops / storage", "",
+            "| dims | scheme | Lap ops | Lap storage | RK4 ops | RK4 storage |", "|---|---|---|---|---|---|"]
+    for d, rows in PAPER.items():
+        for k, v in rows.items():
+            out.append(f"| {d} | {k} | {v[0]} | {v[1]}N | {v[2]} | {v[3]}N |")
+    print("\n".join(out))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ncu", action="store_true")
     ap.add_argument("--parse", nargs=2)
+    ap.add_argument("--report", nargs=3, metavar=("TIME_JSONL", "NCU_JSONL", "PEAKS_JSON"))
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--dims", type=int, nargs="*")
     a = ap.parse_args()
-    if a.parse:
+    if a.report:
+        report(*a.report)
+    elif a.parse:
         parse(*a.parse)
     else:
         run(a.ncu, a.steps, a.reps, a.dims)
