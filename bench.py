@@ -279,9 +279,9 @@ def run_ours(args):
     nbytes = host.numel() * host.element_size() * ws
 
     S_bytes = 8
-    # the fused variant's own minimum traffic: 13 complex transfers per point-step
-    # (stage 1: 2, stage 2: 4, stage 3: 3, stage 4: 4); SURVEY §8(d) counts 16
-    # for the explicit-accumulator form, reported beside it as achieved_16S_equiv
+    # the fused default's own minimum traffic: 13 complex transfers per point-step
+    # (write-light form, stages 2 / 3 / 3 / 5); SURVEY §8(d) counts 16 for the
+    # explicit-accumulator form, reported beside it as achieved_16S_equiv
     transfers = 13
     alg_bytes_per_launch = transfers / 4 * S_bytes * npts_global / ws
     launch_ms = ms / (4 * args.steps)

@@ -124,11 +124,16 @@ nlse2shoc_status nlse2shoc_split(int64_t n_slow, int nranks, int rank, int64_t *
 size_t nlse2shoc_workspace_bytes(nlse2shoc_t);
 
 /* 0 = FUSED (default): one kernel per RK4 stage computes the whole 2SHOC Laplacian (both
- *     steps, D never stored), the RHS and the RK4 stage combine.  2D/3D use the
- *     reconstructed-accumulator form: stage 1 stores only T_A = Psi + k/2 K1, stage 2
- *     forms acc = Psi + (T_A - Psi)/3 + k/3 K2 (= Psi + k/6 K1 + k/3 K2 in exact arithmetic),
- *     stage 3 stores only T_A = Psi + k K3 and stage 4 forms Psi' = acc + (T_A - Psi)/3 +
- *     k/6 K4: 13 field transfers per point-step.
+ *     steps, D never stored), the RHS and the RK4 stage combine, 13 field transfers per
+ *     point-step.  2D/3D: the write-light form (= variant 5); 1D: the
+ *     reconstructed-accumulator form (= variant 6).
+ * 5 = FUSED_WRITE_LIGHT (2D/3D): stages 1-3 store only T_A = Psi + k/2 K1, T_B = Psi + k/2 K2,
+ *     T_C = Psi + k K3 (T_C in the accumulator's buffer); stage 4 forms Psi' = Psi +
+ *     ((T_A - Psi) + 2 (T_B - Psi) + (T_C - Psi))/3 + k/6 K4 (the accumulator is never
+ *     stored: acc = (T_A + 2 T_B)/3 in exact arithmetic).  EUNSUPPORTED in 1D.
+ * 6 = FUSED_RECON: stage 1 stores only T_A = Psi + k/2 K1, stage 2 forms acc = Psi + (T_A -
+ *     Psi)/3 + k/3 K2, stage 3 stores only T_A = Psi + k K3, stage 4 forms Psi' = acc +
+ *     (T_A - Psi)/3 + k/6 K4.
  * 1 = TWO_KERNEL: the paper's single-storage scheme (`2d2shocs1/2`, `3d2shocs`):
  *     kernel A stores D = sum_d delta_d^2 Psi (D_b = lambda_b), kernel B applies step 2 +
  *     RHS + combine.  One more field of workspace (allocated on first use).
@@ -141,7 +146,7 @@ size_t nlse2shoc_workspace_bytes(nlse2shoc_t);
  * 4 = STAGE_PAIRS (temporal blocking): one launch runs stages 1+2 and one
  *     runs stages 3+4 over each tile, the first stage of a pair evaluated on the tile grown by
  *     the stencil radius and kept in shared memory: 7 field transfers per point-step plus the
- *     wider halos.  Results are bit-identical to variant 0.  Psi^{n+1} is written to the T_A
+ *     wider halos.  Results are bit-identical to variant 6.  Psi^{n+1} is written to the T_A
  *     workspace on odd steps and copied back once per call.  2D/3D single-slab handles only
  *     (EUNSUPPORTED otherwise).
  * Variants 1 and 3 are 2SHOC forms: EUNSUPPORTED with the CD scheme.

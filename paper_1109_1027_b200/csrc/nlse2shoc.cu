@@ -321,7 +321,7 @@ template <int DIMS, typename R, int MODE> static nlse2shoc_status set_smem_attr(
 
 template <int DIMS, typename R, int MODE>
 static nlse2shoc_status launch_stream(nlse2shoc_t H, Field &in, const CUtensorMap *tm_psi, const CUtensorMap *tm_acc,
-                                      StageParams<R> P, cudaStream_t st) {
+                                      StageParams<R> P, cudaStream_t st, const CUtensorMap *tm_t3 = nullptr) {
   using C = Cfg<DIMS, R>;
   using LY = Layout<DIMS, R>;
   TRY((set_smem_attr<DIMS, R, MODE>()));
@@ -382,7 +382,7 @@ static nlse2shoc_status launch_stream(nlse2shoc_t H, Field &in, const CUtensorMa
   const CUtensorMap *lo = P.has_lo_halo ? &in.tm_lo : &in.tm;
   const CUtensorMap *hi = P.has_hi_halo ? &in.tm_hi : &in.tm;
   stage_stream_kernel<DIMS, R, MODE><<<G, LY::NTHREADS, smem, st>>>(in.tm, *lo, *hi, tm_psi ? *tm_psi : in.tm,
-                                                                   tm_acc ? *tm_acc : in.tm, P);
+                                                                   tm_acc ? *tm_acc : in.tm, tm_t3 ? *tm_t3 : in.tm, P);
   CUDA_TRY(cudaGetLastError());
   ++H->launches;
   return NLSE2SHOC_OK;
@@ -533,7 +533,14 @@ static nlse2shoc_status launch_two(int, int stage, const cplx<R> *in, const cplx
 //   1: acc = Psi + k/6 K1,  T_A = Psi + k/2 K1        3: acc += k/3 K3,  T_A = Psi + k K3
 //   2: acc += k/3 K2,       T_B = Psi + k/2 K2        4: Psi = acc + k/6 K4
 // s = 5 is the Laplacian (Psi -> L).
-static Field &stage_input(nlse2shoc_t H, Field &psi, int s) { return (s == 1 || s == 5) ? psi : (s == 3 ? H->TB : H->TA); }
+// Write-light combine: the default of 2D/3D handles (variant 0) and variant 5.
+static bool write_light(const nlse2shoc_t H) { return H->dims >= 2 && (H->variant == 0 || H->variant == 5); }
+
+// (write-light: stage 3 writes T_C into acc's buffer, which is stage 4's stencil input)
+static Field &stage_input(nlse2shoc_t H, Field &psi, int s) {
+  if (s == 4 && write_light(H)) return H->acc;
+  return (s == 1 || s == 5) ? psi : (s == 3 ? H->TB : H->TA);
+}
 
 template <int DIMS, typename R, int MODE>
 static nlse2shoc_status launch_mode(nlse2shoc_t H, Field &psi, Field &in, StageParams<R> &P, cudaStream_t st) {
@@ -566,8 +573,29 @@ static nlse2shoc_status launch_stage(nlse2shoc_t H, Field &psi, int s, double dt
   Field &in = stage_input(H, psi, s);
   cplx<R> *pPsi = reinterpret_cast<cplx<R> *>(psi.ptr), *pA = reinterpret_cast<cplx<R> *>(H->TA.ptr),
           *pB = reinterpret_cast<cplx<R> *>(H->TB.ptr), *pAcc = reinterpret_cast<cplx<R> *>(H->acc.ptr);
-  // reconstructed-accumulator form (13 transfers per point-step): variant 0
-  const bool recon = H->variant == 0;
+  // reconstructed-accumulator form (13 transfers per point-step): variant 6, and
+  // variant 0 of 1D handles
+  const bool recon = H->variant == 0 || H->variant == 6;
+  if constexpr (DIMS >= 2) {
+    if (write_light(H)) {  // write-light form: T_A, T_B, T_C; acc never stored
+      switch (s) {
+        case 1:
+          P.cb = R(dt / 2.0); P.out_T = pA;
+          return launch_stream<DIMS, R, M_S1R>(H, in, &psi.tm_pt, &H->acc.tm_pt, P, st);
+        case 2:
+          P.cb = R(dt / 2.0); P.out_T = pB;
+          return launch_stream<DIMS, R, M_S3R>(H, in, &psi.tm_pt, &H->acc.tm_pt, P, st);
+        case 3:
+          P.cb = R(dt); P.out_T = pAcc;  // T_C
+          return launch_stream<DIMS, R, M_S3R>(H, in, &psi.tm_pt, &H->acc.tm_pt, P, st);
+        case 4:
+          P.cb = R(dt / 6.0); P.out_T = pPsi;
+          return launch_stream<DIMS, R, M_S4X>(H, in, &psi.tm_pt, &H->TA.tm_pt, P, st, &H->TB.tm_pt);
+        default:
+          break;
+      }
+    }
+  }
   switch (s) {
     case 1:
       P.ca = R(dt / 6.0); P.cb = R(dt / 2.0); P.out_T = pA; P.out_acc = pAcc;
@@ -677,7 +705,8 @@ static bool overlap_ok(const View &v) {
   if (off) return false;
   bool multi = v.hs.size() > 1;
   for (nlse2shoc_t H : v.hs) {
-    if (H->dims < 2 || (H->variant != 0 && H->variant != 2) || H->nz < 8) return false;
+    if (H->dims < 2 || (H->variant != 0 && H->variant != 2 && H->variant != 5 && H->variant != 6) || H->nz < 8)
+      return false;
     multi = multi || (H->sharded && H->nranks > 1);
   }
   return multi;
@@ -901,7 +930,7 @@ static nlse2shoc_status create_impl(nlse2shoc_t *out, int dims, const int64_t N[
   }
   chk(alloc_field(H, H->TA, true));
   chk(alloc_field(H, H->TB, true));
-  chk(alloc_field(H, H->acc, false));
+  chk(alloc_field(H, H->acc, true));  // halos: stage 4's stencil input in variant 5
   if (st == NLSE2SHOC_OK && H->pitch != H->nx && !H->loop_member) {
     chk(alloc_field(H, H->psiw, true));
     if (st == NLSE2SHOC_OK && dev_malloc(H, &H->Lw, size_t(H->local_elems) * H->S) != cudaSuccess)
@@ -1157,9 +1186,11 @@ size_t nlse2shoc_workspace_bytes(nlse2shoc_t H) {
 nlse2shoc_status nlse2shoc_set_variant(nlse2shoc_t H, int variant) {
   if (!H) return fail(NLSE2SHOC_EINVAL, "NULL handle");
   DeviceGuard dg(H->device);
-  if (variant < 0 || variant > 4)
-    return fail(NLSE2SHOC_EINVAL, "variant must be 0 (fused), 1 (two-kernel), 2 (fused, 16-transfer "
-                                  "accumulator), 3 (two-kernel, multi-storage) or 4 (stage pairs)");
+  if (variant < 0 || variant > 6)
+    return fail(NLSE2SHOC_EINVAL, "variant must be 0 (fused default), 1 (two-kernel), 2 (fused, 16-transfer "
+                                  "accumulator), 3 (two-kernel, multi-storage), 4 (stage pairs), 5 (fused, "
+                                  "write-light) or 6 (fused, reconstructed accumulator)");
+  if (variant == 5 && H->dims < 2) return fail(NLSE2SHOC_EUNSUPPORTED, "variant 5 is 2D/3D");
   if (variant == 4 && (H->dims < 2 || !H->slabs.empty() || H->sharded))
     return fail(NLSE2SHOC_EUNSUPPORTED, "the stage-pair variant needs a single-slab 2D/3D handle");
   if ((variant == 1 || variant == 3) && H->scheme != NLSE2SHOC_SCHEME_2SHOC)

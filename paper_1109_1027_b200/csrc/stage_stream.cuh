@@ -37,7 +37,9 @@ namespace nlse {
 // ((T_A - Psi)/3 = k/6 K1 in exact arithmetic).  M_LAP: the Laplacian alone.
 // M_S3R / M_S4R: stage 3 stores only T_A = Psi + k K3 and stage 4 forms
 // Psi' = acc + (T_A - Psi)/3 + k/6 K4 ((T_A - Psi)/3 = k/3 K3): 13 transfers in all.
-enum Mode { M_S1 = 1, M_S2 = 2, M_S3 = 3, M_S4 = 4, M_LAP = 5, M_S1R = 6, M_S2R = 7, M_S3R = 8, M_S4R = 9 };
+// M_S4X (variant 5): stage 4 of the write-light form: Psi' = Psi + ((T_A - Psi) + 2 (T_B - Psi) +
+// (T_C - Psi)) / 3 + k/6 K4 from the stencil input T_C and pointwise Psi, T_A, T_B.
+enum Mode { M_S1 = 1, M_S2 = 2, M_S3 = 3, M_S4 = 4, M_LAP = 5, M_S1R = 6, M_S2R = 7, M_S3R = 8, M_S4R = 9, M_S4X = 10 };
 
 // Tile configuration per (dims, precision).  W = smem row width in complex elements
 // (tile + 2+2 halo, rounded so that it splits into NBOX equal TMA boxes); every TMA
@@ -68,7 +70,9 @@ template <int SLOT_B, int PT_B> struct Rings {
   static constexpr int RP1 = mn(12, (BUDGET - RT1 * SLOT_B) / PT_B);
   static constexpr int RT2 = 4 + cdiv(NLSE_RT2_KB * 1024, SLOT_B);
   static constexpr int RP2 = mn(8, (BUDGET - RT2 * SLOT_B) / (2 * PT_B));
-  static_assert(RT0 >= 5 && RP1 >= 2 && RP2 >= 2, "shared-memory budget too small for the tile");
+  static constexpr int RT3 = mn(RT2, (BUDGET - 6 * PT_B) / SLOT_B);  // keep >= 2 slots of 3 tiles
+  static constexpr int RP3 = mn(8, (BUDGET - RT3 * SLOT_B) / (3 * PT_B));
+  static_assert(RT0 >= 5 && RP1 >= 2 && RP2 >= 2 && RP3 >= 2, "shared-memory budget too small for the tile");
 };
 // 3D tiles: 28 rows (y-halo overhead 32/28) handled by 14 consumer warps x 2 rows each;
 // chosen by a sweep over (TY, warps, rows/warp) on C4 (scripts/sweep.py).
@@ -108,65 +112,65 @@ template <> struct Cfg<3, double> : Rings<36 * (NLSE3D_TY + 4) * 16, 32 * NLSE3D
 #if NLSE2D_PRESET == 0
 template <> struct Cfg<2, float> {
   static constexpr int TX = 512, TY = 1, PPX = 2, RPW = 1, NCW = 8, NBOX = 3, NBOXP = 2, W = 528;
-  static constexpr int RT0 = 40, RT1 = 24, RP1 = 20, RT2 = 20, RP2 = 12;
+  static constexpr int RT0 = 40, RT1 = 24, RP1 = 20, RT2 = 20, RP2 = 12, RT3 = 20, RP3 = 8;
 };
 template <> struct Cfg<2, double> {
   static constexpr int TX = 256, TY = 1, PPX = 1, RPW = 1, NCW = 8, NBOX = 3, NBOXP = 2, W = 264;
-  static constexpr int RT0 = 40, RT1 = 24, RP1 = 20, RT2 = 20, RP2 = 12;
+  static constexpr int RT0 = 40, RT1 = 24, RP1 = 20, RT2 = 20, RP2 = 12, RT3 = 20, RP3 = 8;
 };
 #elif NLSE2D_PRESET == 1
 template <> struct Cfg<2, float> {
   static constexpr int TX = 512, TY = 1, PPX = 2, RPW = 1, NCW = 8, NBOX = 3, NBOXP = 2, W = 528;
-  static constexpr int RT0 = 20, RT1 = 12, RP1 = 10, RT2 = 10, RP2 = 6;
+  static constexpr int RT0 = 20, RT1 = 12, RP1 = 10, RT2 = 10, RP2 = 6, RT3 = 10, RP3 = 4;
 };
 template <> struct Cfg<2, double> {
   static constexpr int TX = 256, TY = 1, PPX = 1, RPW = 1, NCW = 8, NBOX = 3, NBOXP = 2, W = 264;
-  static constexpr int RT0 = 20, RT1 = 12, RP1 = 10, RT2 = 10, RP2 = 6;
+  static constexpr int RT0 = 20, RT1 = 12, RP1 = 10, RT2 = 10, RP2 = 6, RT3 = 10, RP3 = 4;
 };
 #elif NLSE2D_PRESET == 2
 template <> struct Cfg<2, float> {
   static constexpr int TX = 1024, TY = 1, PPX = 4, RPW = 1, NCW = 8, NBOX = 5, NBOXP = 4, W = 1040;
-  static constexpr int RT0 = 24, RT1 = 12, RP1 = 12, RT2 = 10, RP2 = 7;
+  static constexpr int RT0 = 24, RT1 = 12, RP1 = 12, RT2 = 10, RP2 = 7, RT3 = 10, RP3 = 4;
 };
 template <> struct Cfg<2, double> {
   static constexpr int TX = 512, TY = 1, PPX = 2, RPW = 1, NCW = 8, NBOX = 5, NBOXP = 4, W = 520;
-  static constexpr int RT0 = 24, RT1 = 12, RP1 = 12, RT2 = 10, RP2 = 7;
+  static constexpr int RT0 = 24, RT1 = 12, RP1 = 12, RT2 = 10, RP2 = 7, RT3 = 10, RP3 = 4;
 };
 #elif NLSE2D_PRESET == 4
 template <> struct Cfg<2, float> {
   static constexpr int TX = 2048, TY = 1, PPX = 8, RPW = 1, NCW = 8, NBOX = 10, NBOXP = 8, W = 2080;
-  static constexpr int RT0 = 12, RT1 = 6, RP1 = 6, RT2 = 6, RP2 = 3;
+  static constexpr int RT0 = 12, RT1 = 6, RP1 = 6, RT2 = 6, RP2 = 3, RT3 = 6, RP3 = 2;
 };
 template <> struct Cfg<2, double> {
   static constexpr int TX = 1024, TY = 1, PPX = 4, RPW = 1, NCW = 8, NBOX = 10, NBOXP = 8, W = 1040;
-  static constexpr int RT0 = 12, RT1 = 6, RP1 = 6, RT2 = 6, RP2 = 3;
+  static constexpr int RT0 = 12, RT1 = 6, RP1 = 6, RT2 = 6, RP2 = 3, RT3 = 6, RP3 = 2;
 };
 #elif NLSE2D_PRESET == 5
 template <> struct Cfg<2, float> {
   static constexpr int TX = 2048, TY = 1, PPX = 4, RPW = 1, NCW = 16, NBOX = 10, NBOXP = 8, W = 2080;
-  static constexpr int RT0 = 12, RT1 = 6, RP1 = 6, RT2 = 6, RP2 = 3;
+  static constexpr int RT0 = 12, RT1 = 6, RP1 = 6, RT2 = 6, RP2 = 3, RT3 = 6, RP3 = 2;
 };
 template <> struct Cfg<2, double> {
   static constexpr int TX = 1024, TY = 1, PPX = 2, RPW = 1, NCW = 16, NBOX = 10, NBOXP = 8, W = 1040;
-  static constexpr int RT0 = 12, RT1 = 6, RP1 = 6, RT2 = 6, RP2 = 3;
+  static constexpr int RT0 = 12, RT1 = 6, RP1 = 6, RT2 = 6, RP2 = 3, RT3 = 6, RP3 = 2;
 };
 #elif NLSE2D_PRESET == 6
 template <> struct Cfg<2, float> {
   static constexpr int TX = 1024, TY = 1, PPX = 4, RPW = 1, NCW = 8, NBOX = 5, NBOXP = 4, W = 1040;
-  static constexpr int RT0 = 24, RT1 = 14, RP1 = 10, RT2 = 12, RP2 = 6;
+  static constexpr int RT0 = 24, RT1 = 14, RP1 = 10, RT2 = 12, RP2 = 6, RT3 = 12, RP3 = 4;
 };
 template <> struct Cfg<2, double> {
   static constexpr int TX = 512, TY = 1, PPX = 2, RPW = 1, NCW = 8, NBOX = 5, NBOXP = 4, W = 520;
-  static constexpr int RT0 = 24, RT1 = 14, RP1 = 10, RT2 = 12, RP2 = 6;
+  static constexpr int RT0 = 24, RT1 = 14, RP1 = 10, RT2 = 12, RP2 = 6, RT3 = 12, RP3 = 4;
 };
 #else
 template <> struct Cfg<2, float> {
   static constexpr int TX = 1024, TY = 1, PPX = 2, RPW = 1, NCW = 16, NBOX = 5, NBOXP = 4, W = 1040;
-  static constexpr int RT0 = 24, RT1 = 12, RP1 = 12, RT2 = 10, RP2 = 7;
+  static constexpr int RT0 = 24, RT1 = 12, RP1 = 12, RT2 = 10, RP2 = 7, RT3 = 10, RP3 = 4;
 };
 template <> struct Cfg<2, double> {
   static constexpr int TX = 512, TY = 1, PPX = 1, RPW = 1, NCW = 16, NBOX = 5, NBOXP = 4, W = 520;
-  static constexpr int RT0 = 24, RT1 = 12, RP1 = 12, RT2 = 10, RP2 = 7;
+  static constexpr int RT0 = 24, RT1 = 12, RP1 = 12, RT2 = 10, RP2 = 7, RT3 = 10, RP3 = 4;
 };
 #endif
 
@@ -224,20 +228,24 @@ template <int DIMS, typename R> struct Layout {
   static_assert(C::NBOXP == 1 || (BWP * 8) % 128 == 0, "P sub-boxes 128-byte aligned");
   static_assert((C::TX / C::PPX) * (C::TY / C::RPW) == C::NCW * 32, "thread map");
   template <int MODE> __host__ __device__ static constexpr bool needs_psi() {
-    return MODE == M_S2 || MODE == M_S3 || MODE == M_S2R || MODE == M_S3R || MODE == M_S4R;
+    return MODE == M_S2 || MODE == M_S3 || MODE == M_S2R || MODE == M_S3R || MODE == M_S4R || MODE == M_S4X;
   }
+  // third pointwise tile (M_S4X: T_B; its second tile, in the acc position, is T_A)
+  template <int MODE> __host__ __device__ static constexpr bool needs_t3() { return MODE == M_S4X; }
   template <int MODE> __host__ __device__ static constexpr bool writes_acc() {
     return MODE == M_S1 || MODE == M_S2 || MODE == M_S3 || MODE == M_S2R;
   }
   template <int MODE> __host__ __device__ static constexpr bool needs_acc() {
-    return MODE == M_S2 || MODE == M_S3 || MODE == M_S4 || MODE == M_S4R;
+    return MODE == M_S2 || MODE == M_S3 || MODE == M_S4 || MODE == M_S4R || MODE == M_S4X;
   }
-  template <int MODE> __host__ __device__ static constexpr int pa_tiles() { return (needs_psi<MODE>() ? 1 : 0) + (needs_acc<MODE>() ? 1 : 0); }
+  template <int MODE> __host__ __device__ static constexpr int pa_tiles() {
+    return (needs_psi<MODE>() ? 1 : 0) + (needs_acc<MODE>() ? 1 : 0) + (needs_t3<MODE>() ? 1 : 0);
+  }
   template <int MODE> __host__ __device__ static constexpr int rt() {
-    return pa_tiles<MODE>() == 0 ? C::RT0 : (pa_tiles<MODE>() == 1 ? C::RT1 : C::RT2);
+    return pa_tiles<MODE>() == 0 ? C::RT0 : (pa_tiles<MODE>() == 1 ? C::RT1 : (pa_tiles<MODE>() == 2 ? C::RT2 : C::RT3));
   }
   template <int MODE> __host__ __device__ static constexpr int rp() {
-    return pa_tiles<MODE>() == 0 ? 0 : (pa_tiles<MODE>() == 1 ? C::RP1 : C::RP2);
+    return pa_tiles<MODE>() == 0 ? 0 : (pa_tiles<MODE>() == 1 ? C::RP1 : (pa_tiles<MODE>() == 2 ? C::RP2 : C::RP3));
   }
   template <int MODE> __host__ __device__ static constexpr size_t smem_bytes() {
     return size_t(rt<MODE>()) * SLOT_BYTES + size_t(rp<MODE>()) * pa_tiles<MODE>() * PTILE_BYTES +
@@ -297,7 +305,8 @@ template <int DIMS, typename R, int MODE>
 __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
     stage_stream_kernel(const __grid_constant__ CUtensorMap tm_T, const __grid_constant__ CUtensorMap tm_lo,
                         const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_psi,
-                        const __grid_constant__ CUtensorMap tm_acc, const StageParams<R> P) {
+                        const __grid_constant__ CUtensorMap tm_acc, const __grid_constant__ CUtensorMap tm_t3,
+                        const StageParams<R> P) {
   using C = Cfg<DIMS, R>;
   using LY = Layout<DIMS, R>;
   using CT = cplx<R>;
@@ -306,6 +315,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
   constexpr int RT = LY::template rt<MODE>(), RP = LY::template rp<MODE>();
   constexpr int RPM = RP > 0 ? RP : 1;  // modulus for the (unused when RP = 0) P-ring counters
   constexpr int ACC_OFF = LY::template needs_psi<MODE>() ? LY::PTILE : 0;  // acc tile offset in a P slot
+  constexpr int T3_OFF = ACC_OFF + LY::PTILE;                                // third tile (M_S4X)
 
   // Dynamic shared memory starts 1 KB-aligned; deriving every pointer from smem_raw by
   // plain offsets keeps them in the shared state space (LDS, 32-bit addressing).
@@ -343,6 +353,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
       if (NPA) {
         if (LY::template needs_psi<MODE>()) prefetch_tmap(&tm_psi);
         if (LY::template needs_acc<MODE>()) prefetch_tmap(&tm_acc);
+        if (LY::template needs_t3<MODE>()) prefetch_tmap(&tm_t3);
       }
       // stencil-input planes are re-read (halos) by neighbouring tiles: keep them in L2;
       // Psi^n / acc tiles are read exactly once: evict first.
@@ -433,16 +444,18 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
           mbar_arrive_expect_tx(&fullP[slot], NPA * LY::PTILE_BYTES);
           CT *dst = pring + size_t(slot) * NPA * LY::PTILE;
 #pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const bool want = q == 0 ? LY::template needs_psi<MODE>() : LY::template needs_acc<MODE>();
+          for (int q = 0; q < 3; ++q) {
+            const bool want = q == 0   ? LY::template needs_psi<MODE>()
+                              : q == 1 ? LY::template needs_acc<MODE>()
+                                       : LY::template needs_t3<MODE>();
             if (!want) continue;
-            const CUtensorMap *m = q == 0 ? &tm_psi : &tm_acc;
+            const CUtensorMap *m = q == 0 ? &tm_psi : (q == 1 ? &tm_acc : &tm_t3);
 #pragma unroll
             for (int b = 0; b < C::NBOXP; ++b) {
               const int c0 = x0 * LY::EPC + b * LY::BWP;
-              char *d = reinterpret_cast<char *>(dst + (q == 0 ? 0 : ACC_OFF)) + b * LY::BWP * 8;
+              char *d = reinterpret_cast<char *>(dst + (q == 0 ? 0 : (q == 1 ? ACC_OFF : T3_OFF))) + b * LY::BWP * 8;
               // Psi^n is re-read by the next stage (L2 reuse); acc is not
-              const uint64_t pol = q == 0 ? pol_stream : pol_acc;
+              const uint64_t pol = q == 1 ? pol_acc : pol_stream;
               if (DIMS == 3) tma_load_3d_hint(d, m, &fullP[slot], c0, y0, k, pol);
               else tma_load_2d_hint(d, m, &fullP[slot], c0, k, pol);
             }
@@ -647,6 +660,8 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
         const int poff = (ly0 + r) * TX + lx0;
         if (LY::template needs_psi<MODE>()) lds_run<R, PPX>(pa + poff, psv);
         if (LY::template needs_acc<MODE>()) lds_run<R, PPX>(pa + ACC_OFF + poff, acv);
+        CT t3v[PPX];
+        if (LY::template needs_t3<MODE>()) lds_run<R, PPX>(pa + T3_OFF + poff, t3v);
 
         CT oT[PPX], oA[PPX];
         bool valid[PPX];
@@ -696,6 +711,10 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
             oT[q] = iaxpy(psv[q], cb, tF);
           } else if (MODE == M_S4R) {
             oT[q] = iaxpy(axpy(acv[q], R(1.0 / 3.0), c - psv[q]), cb, tF);
+          } else if (MODE == M_S4X) {
+            // acc = (T_A + 2 T_B) / 3 in exact arithmetic; the differences keep it to O(k)
+            const CT dsum = axpy(acv[q] - psv[q], R(2), t3v[q] - psv[q]) + (c - psv[q]);
+            oT[q] = iaxpy(axpy(psv[q], R(1.0 / 3.0), dsum), cb, tF);
           } else if (MODE == M_S2 || MODE == M_S3) {
             oA[q] = iaxpy(acv[q], ca, tF);
             oT[q] = iaxpy(psv[q], cb, tF);
@@ -789,6 +808,8 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
         CT psv[PPX], acv[PPX];
         if (LY::template needs_psi<MODE>()) lds_run<R, PPX>(pa + r * TX, psv);
         if (LY::template needs_acc<MODE>()) lds_run<R, PPX>(pa + ACC_OFF + r * TX, acv);
+        CT t3v[PPX];
+        if (LY::template needs_t3<MODE>()) lds_run<R, PPX>(pa + T3_OFF + r * TX, t3v);
         CT oT[PPX], oA[PPX];
 #pragma unroll
         for (int q = 0; q < PPX; ++q) {
@@ -821,6 +842,10 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
             oT[q] = iaxpy(psv[q], cb, tF);
           } else if (MODE == M_S4R) {
             oT[q] = iaxpy(axpy(acv[q], R(1.0 / 3.0), c - psv[q]), cb, tF);
+          } else if (MODE == M_S4X) {
+            // acc = (T_A + 2 T_B) / 3 in exact arithmetic; the differences keep it to O(k)
+            const CT dsum = axpy(acv[q] - psv[q], R(2), t3v[q] - psv[q]) + (c - psv[q]);
+            oT[q] = iaxpy(axpy(psv[q], R(1.0 / 3.0), dsum), cb, tF);
           } else if (MODE == M_S2 || MODE == M_S3) {
             oA[q] = iaxpy(acv[q], ca, tF);
             oT[q] = iaxpy(psv[q], cb, tF);

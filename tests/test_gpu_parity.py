@@ -57,11 +57,11 @@ def test_laplacian_parity(dims, n, dtype, bc, V, variant):
     assert H.rel_l2(L.cpu().numpy(), Lo) <= tol
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6])
 @pytest.mark.parametrize("dims,n,dtype,bc,V", CASES[::2])
 def test_rk4_parity_10_steps(dims, n, dtype, bc, V, variant):
-    if variant == 4 and dims == 1:
-        pytest.skip("stage pairs: 2D/3D only")
+    if variant in (4, 5) and dims == 1:
+        pytest.skip("stage pairs / write-light form: 2D/3D only")
     w = _small(dims, n, bc, dtype, V)
     S = H.gpu_solver(w, dtype, variant)
     psi = H.psi0_host(w, dtype)
@@ -267,7 +267,7 @@ def _core_box_work(w, lo, cnt):
     return wc
 
 
-@pytest.mark.parametrize("dtype,variant", [("c64", 0), ("c64", 2), ("c128", 0)])
+@pytest.mark.parametrize("dtype,variant", [("c64", 0), ("c64", 2), ("c64", 6), ("c128", 0), ("c128", 6)])
 def test_C4_core_box_full_step_count(dtype, variant):
     """C4 at its stated step count (100) on a 96^3 box around the ring core with C4's own
     spacing (SURVEY A7 analogue): the whole-field parity the north star states, for the

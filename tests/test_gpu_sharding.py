@@ -40,7 +40,7 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 6])
 @pytest.mark.parametrize("nslabs", [2, 3, 7])
 @pytest.mark.parametrize("dims,n,bc,dtype,V", CASES)
 def test_loopback_bitwise_equal(dims, n, bc, dtype, V, nslabs, variant):
