@@ -6,7 +6,8 @@ non-compact scheme and the 2SHOC single-storage ("1X") and multi-storage ("2X"/"
 Here each realisation in the library is timed on one B200 at a paper-sized workload:
 
   fused-13  variant 0: one kernel per stage, wide 2SHOC form (= the non-compact stencil in the
-            interior), reconstructed accumulator (13 field transfers per point-step)
+            interior), write-light combine in 2D/3D (13 field transfers per point-step)
+  fused-13r variant 6: as fused-13 with the reconstructed accumulator (13 transfers)
   fused-16  variant 2: as fused-13 with the explicit accumulator (16 transfers)
   2k-1X     variant 1: the paper's single-storage two-step scheme, D stored (`2d2shocs1/2`)
   2k-MS     variant 3: the paper's multi-storage scheme, D_d per axis stored (`*2shocMs1/2`)
@@ -32,8 +33,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
-ROWS = [("fused-13", 0, "2shoc"), ("fused-16", 2, "2shoc"), ("2k-1X", 1, "2shoc"), ("2k-MS", 3, "2shoc"),
-        ("CD", 0, "cd"), ("pairs", 4, "2shoc")]
+ROWS = [("fused-13", 0, "2shoc"), ("fused-13r", 6, "2shoc"), ("fused-16", 2, "2shoc"), ("2k-1X", 1, "2shoc"),
+        ("2k-MS", 3, "2shoc"), ("CD", 0, "cd"), ("pairs", 4, "2shoc")]
 
 # paper's static counts (Tables 3-5): (Laplacian ops, Laplacian storage, RK4 ops, RK4 storage)
 PAPER = {
@@ -51,7 +52,7 @@ def workloads():
 
 
 def rows_for(dims):
-    return [r for r in ROWS if not (dims == 1 and r[1] in (3, 4))]  # 1D: MS == 1X; pairs are 2D/3D
+    return [r for r in ROWS if not (dims == 1 and r[1] in (3, 4, 6))]  # 1D: MS == 1X, 0 == 6; pairs 2D/3D
 
 
 def run(ncu: bool, steps: int, reps: int, only):
