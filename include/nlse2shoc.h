@@ -125,12 +125,11 @@ size_t nlse2shoc_workspace_bytes(nlse2shoc_t);
 
 /* 0 = FUSED (default): one kernel per RK4 stage computes the whole 2SHOC Laplacian (both
  *     steps, D never stored), the RHS and the RK4 stage combine, 13 field transfers per
- *     point-step.  2D/3D: the write-light form (= variant 5); 1D: the
- *     reconstructed-accumulator form (= variant 6).
- * 5 = FUSED_WRITE_LIGHT (2D/3D): stages 1-3 store only T_A = Psi + k/2 K1, T_B = Psi + k/2 K2,
+ *     point-step, in the write-light form (= variant 5).
+ * 5 = FUSED_WRITE_LIGHT: stages 1-3 store only T_A = Psi + k/2 K1, T_B = Psi + k/2 K2,
  *     T_C = Psi + k K3 (T_C in the accumulator's buffer); stage 4 forms Psi' = Psi +
  *     ((T_A - Psi) + 2 (T_B - Psi) + (T_C - Psi))/3 + k/6 K4 (the accumulator is never
- *     stored: acc = (T_A + 2 T_B)/3 in exact arithmetic).  EUNSUPPORTED in 1D.
+ *     stored: acc = (T_A + 2 T_B)/3 in exact arithmetic).
  * 6 = FUSED_RECON: stage 1 stores only T_A = Psi + k/2 K1, stage 2 forms acc = Psi + (T_A -
  *     Psi)/3 + k/3 K2, stage 3 stores only T_A = Psi + k K3, stage 4 forms Psi' = acc +
  *     (T_A - Psi)/3 + k/6 K4.

@@ -352,10 +352,6 @@ static nlse2shoc_status launch_stream(nlse2shoc_t H, Field &in, const CUtensorMa
   P.nchunk = best;
   P.ntiles = ncol * best;
   const int G = std::min(G0, P.ntiles);
-  // stages 2 and 4 walk the tiles backwards: the planes the previous stage wrote last are
-  // still in L2 when this stage starts (NLSE_NO_REV=1 disables)
-  static const bool no_rev = getenv("NLSE_NO_REV") != nullptr;
-  P.rev = (!no_rev && (MODE == M_S2 || MODE == M_S4 || MODE == M_S2R || MODE == M_S4R)) ? 1 : 0;
   // neighbour coupling (NLSE_LEAD=0 disables): per-tile progress words, epoch-tagged
   static const int lead = getenv("NLSE_LEAD") ? atoi(getenv("NLSE_LEAD")) : 0;
   static const int rbar = getenv("NLSE_RBAR") ? atoi(getenv("NLSE_RBAR")) : 0;
@@ -461,10 +457,8 @@ static nlse2shoc_status rk4_pairs(nlse2shoc_t H, Field &psi, double dt, int64_t 
 
 template <typename R, int MODE>
 static nlse2shoc_status launch_line(nlse2shoc_t H, const void *in, const void *psi, const void *acc, StageParams<R> P,
-                                    cudaStream_t st) {
+                                    cudaStream_t st, const void *t3 = nullptr) {
   const int threads = 256;
-  static const bool no_rev = getenv("NLSE_NO_REV") != nullptr;
-  P.rev = (!no_rev && (MODE == M_S2 || MODE == M_S4 || MODE == M_S2R || MODE == M_S4R)) ? 1 : 0;
   // complex128: the grid-stride kernel (L1 serves the stencil overlap) measured faster than the
   // shared-memory tiles on C2 (0.191 vs 0.205-0.230 ms/step); complex64: tiles of 256 points
   // (C2 0.110 ms; 512 / 1024 / 2048-point tiles 0.128 / 0.119 / 0.115, grid-stride 0.125)
@@ -478,13 +472,13 @@ static nlse2shoc_status launch_line(nlse2shoc_t H, const void *in, const void *p
     const int64_t blocks = std::min<int64_t>((H->nx + threads - 1) / threads, int64_t(H->num_sms) * 8);
     stage_line_kernel<R, MODE><<<int(blocks), threads, 0, st>>>(
         reinterpret_cast<const cplx<R> *>(in), reinterpret_cast<const cplx<R> *>(psi),
-        reinterpret_cast<const cplx<R> *>(acc), P);
+        reinterpret_cast<const cplx<R> *>(acc), reinterpret_cast<const cplx<R> *>(t3), P);
   } else {
     constexpr int PT = NLSE_LINE_PT;
     const int64_t blocks = (H->nx + threads * PT - 1) / (threads * PT);
     line_tile_kernel<R, MODE, PT><<<int(blocks), threads, 0, st>>>(
         reinterpret_cast<const cplx<R> *>(in), reinterpret_cast<const cplx<R> *>(psi),
-        reinterpret_cast<const cplx<R> *>(acc), P);
+        reinterpret_cast<const cplx<R> *>(acc), reinterpret_cast<const cplx<R> *>(t3), P);
   }
   CUDA_TRY(cudaGetLastError());
   ++H->launches;
@@ -534,7 +528,7 @@ static nlse2shoc_status launch_two(int, int stage, const cplx<R> *in, const cplx
 //   2: acc += k/3 K2,       T_B = Psi + k/2 K2        4: Psi = acc + k/6 K4
 // s = 5 is the Laplacian (Psi -> L).
 // Write-light combine: the default of 2D/3D handles (variant 0) and variant 5.
-static bool write_light(const nlse2shoc_t H) { return H->dims >= 2 && (H->variant == 0 || H->variant == 5); }
+static bool write_light(const nlse2shoc_t H) { return H->variant == 0 || H->variant == 5; }
 
 // (write-light: stage 3 writes T_C into acc's buffer, which is stage 4's stencil input)
 static Field &stage_input(nlse2shoc_t H, Field &psi, int s) {
@@ -570,30 +564,36 @@ template <int DIMS, typename R>
 static nlse2shoc_status launch_stage(nlse2shoc_t H, Field &psi, int s, double dt, void *L, cudaStream_t st) {
   StageParams<R> P;
   fill_params<R>(H, P);
+  // stages 2 and 4 walk the grid backwards: the planes the previous stage wrote last are still
+  // in L2 when this stage starts (NLSE_NO_REV=1 disables)
+  static const bool no_rev = getenv("NLSE_NO_REV") != nullptr;
+  P.rev = (!no_rev && (s == 2 || s == 4)) ? 1 : 0;
   Field &in = stage_input(H, psi, s);
   cplx<R> *pPsi = reinterpret_cast<cplx<R> *>(psi.ptr), *pA = reinterpret_cast<cplx<R> *>(H->TA.ptr),
           *pB = reinterpret_cast<cplx<R> *>(H->TB.ptr), *pAcc = reinterpret_cast<cplx<R> *>(H->acc.ptr);
-  // reconstructed-accumulator form (13 transfers per point-step): variant 6, and
-  // variant 0 of 1D handles
-  const bool recon = H->variant == 0 || H->variant == 6;
-  if constexpr (DIMS >= 2) {
-    if (write_light(H)) {  // write-light form: T_A, T_B, T_C; acc never stored
-      switch (s) {
-        case 1:
-          P.cb = R(dt / 2.0); P.out_T = pA;
-          return launch_stream<DIMS, R, M_S1R>(H, in, &psi.tm_pt, &H->acc.tm_pt, P, st);
-        case 2:
-          P.cb = R(dt / 2.0); P.out_T = pB;
-          return launch_stream<DIMS, R, M_S3R>(H, in, &psi.tm_pt, &H->acc.tm_pt, P, st);
-        case 3:
-          P.cb = R(dt); P.out_T = pAcc;  // T_C
-          return launch_stream<DIMS, R, M_S3R>(H, in, &psi.tm_pt, &H->acc.tm_pt, P, st);
-        case 4:
-          P.cb = R(dt / 6.0); P.out_T = pPsi;
+  // reconstructed-accumulator form (13 transfers per point-step): variant 6
+  const bool recon = H->variant == 6;
+  if (write_light(H)) {  // write-light form: T_A, T_B, T_C; acc never stored
+    switch (s) {
+      case 1:
+        P.cb = R(dt / 2.0); P.out_T = pA;
+        if constexpr (DIMS >= 2) return launch_stream<DIMS, R, M_S1R>(H, in, &psi.tm_pt, &H->acc.tm_pt, P, st);
+        else return launch_line<R, M_S1R>(H, in.ptr, psi.ptr, H->acc.ptr, P, st);
+      case 2:
+        P.cb = R(dt / 2.0); P.out_T = pB;
+        if constexpr (DIMS >= 2) return launch_stream<DIMS, R, M_S3R>(H, in, &psi.tm_pt, &H->acc.tm_pt, P, st);
+        else return launch_line<R, M_S3R>(H, in.ptr, psi.ptr, H->acc.ptr, P, st);
+      case 3:
+        P.cb = R(dt); P.out_T = pAcc;  // T_C
+        if constexpr (DIMS >= 2) return launch_stream<DIMS, R, M_S3R>(H, in, &psi.tm_pt, &H->acc.tm_pt, P, st);
+        else return launch_line<R, M_S3R>(H, in.ptr, psi.ptr, H->acc.ptr, P, st);
+      case 4:
+        P.cb = R(dt / 6.0); P.out_T = pPsi;
+        if constexpr (DIMS >= 2)
           return launch_stream<DIMS, R, M_S4X>(H, in, &psi.tm_pt, &H->TA.tm_pt, P, st, &H->TB.tm_pt);
-        default:
-          break;
-      }
+        else return launch_line<R, M_S4X>(H, in.ptr, psi.ptr, H->TA.ptr, P, st, H->TB.ptr);
+      default:
+        break;
     }
   }
   switch (s) {
@@ -1190,7 +1190,6 @@ nlse2shoc_status nlse2shoc_set_variant(nlse2shoc_t H, int variant) {
     return fail(NLSE2SHOC_EINVAL, "variant must be 0 (fused default), 1 (two-kernel), 2 (fused, 16-transfer "
                                   "accumulator), 3 (two-kernel, multi-storage), 4 (stage pairs), 5 (fused, "
                                   "write-light) or 6 (fused, reconstructed accumulator)");
-  if (variant == 5 && H->dims < 2) return fail(NLSE2SHOC_EUNSUPPORTED, "variant 5 is 2D/3D");
   if (variant == 4 && (H->dims < 2 || !H->slabs.empty() || H->sharded))
     return fail(NLSE2SHOC_EUNSUPPORTED, "the stage-pair variant needs a single-slab 2D/3D handle");
   if ((variant == 1 || variant == 3) && H->scheme != NLSE2SHOC_SCHEME_2SHOC)

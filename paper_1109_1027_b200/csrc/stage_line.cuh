@@ -68,7 +68,8 @@ __device__ __forceinline__ cplx<R> line_point(const cplx<R> *__restrict__ Tin, i
 
 template <typename R, int MODE>
 __global__ void __launch_bounds__(256) stage_line_kernel(const cplx<R> *__restrict__ Tin, const cplx<R> *__restrict__ psi,
-                                                         const cplx<R> *__restrict__ acc, const StageParams<R> P) {
+                                                         const cplx<R> *__restrict__ acc, const cplx<R> *__restrict__ t3,
+                                                         const StageParams<R> P) {
   using CT = cplx<R>;
   const int n = P.nx;
   for (int64_t i0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i0 < n; i0 += int64_t(gridDim.x) * blockDim.x) {
@@ -90,6 +91,10 @@ __global__ void __launch_bounds__(256) stage_line_kernel(const cplx<R> *__restri
       P.out_T[i] = iaxpy(psi[i], P.cb, t);
     } else if (MODE == M_S4R) {
       P.out_T[i] = iaxpy(axpy(acc[i], R(1.0 / 3.0), c - psi[i]), P.cb, t);
+    } else if (MODE == M_S4X) {  // write-light stage 4: acc holds T_A, t3 holds T_B
+      const CT ps = psi[i];
+      const CT dsum = axpy(acc[i] - ps, R(2), t3[i] - ps) + (c - ps);
+      P.out_T[i] = iaxpy(axpy(ps, R(1.0 / 3.0), dsum), P.cb, t);
     } else if (MODE == M_S2 || MODE == M_S3) {
       P.out_acc[i] = iaxpy(acc[i], P.ca, t);
       P.out_T[i] = iaxpy(psi[i], P.cb, t);
@@ -105,7 +110,8 @@ __global__ void __launch_bounds__(256) stage_line_kernel(const cplx<R> *__restri
 // stage_line_kernel.
 template <typename R, int MODE, int PT>
 __global__ void __launch_bounds__(256) line_tile_kernel(const cplx<R> *__restrict__ Tin, const cplx<R> *__restrict__ psi,
-                                                        const cplx<R> *__restrict__ acc, const StageParams<R> P) {
+                                                        const cplx<R> *__restrict__ acc, const cplx<R> *__restrict__ t3,
+                                                        const StageParams<R> P) {
   using CT = cplx<R>;
   constexpr int TILE = 256 * PT;
   __shared__ __align__(16) CT sT[TILE + 8];  // sT[k] = Tin[t0 - 4 + k]
@@ -145,6 +151,10 @@ __global__ void __launch_bounds__(256) line_tile_kernel(const cplx<R> *__restric
       P.out_T[i] = iaxpy(psi[i], P.cb, t);
     } else if (MODE == M_S4R) {
       P.out_T[i] = iaxpy(axpy(acc[i], R(1.0 / 3.0), c - psi[i]), P.cb, t);
+    } else if (MODE == M_S4X) {  // write-light stage 4: acc holds T_A, t3 holds T_B
+      const CT ps = psi[i];
+      const CT dsum = axpy(acc[i] - ps, R(2), t3[i] - ps) + (c - ps);
+      P.out_T[i] = iaxpy(axpy(ps, R(1.0 / 3.0), dsum), P.cb, t);
     } else if (MODE == M_S2 || MODE == M_S3) {
       P.out_acc[i] = iaxpy(acc[i], P.ca, t);
       P.out_T[i] = iaxpy(psi[i], P.cb, t);

@@ -60,8 +60,8 @@ def test_laplacian_parity(dims, n, dtype, bc, V, variant):
 @pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6])
 @pytest.mark.parametrize("dims,n,dtype,bc,V", CASES[::2])
 def test_rk4_parity_10_steps(dims, n, dtype, bc, V, variant):
-    if variant in (4, 5) and dims == 1:
-        pytest.skip("stage pairs / write-light form: 2D/3D only")
+    if variant == 4 and dims == 1:
+        pytest.skip("stage pairs: 2D/3D only")
     w = _small(dims, n, bc, dtype, V)
     S = H.gpu_solver(w, dtype, variant)
     psi = H.psi0_host(w, dtype)
