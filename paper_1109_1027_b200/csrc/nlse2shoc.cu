@@ -375,6 +375,7 @@ static nlse2shoc_status launch_stream(nlse2shoc_t H, Field &in, const CUtensorMa
     static const int pair = getenv("NLSE_LEAD_PAIR") ? atoi(getenv("NLSE_LEAD_PAIR")) : 1;
     P.lead_pair = pair;
   }
+  P.in_T = reinterpret_cast<const cplx<R> *>(in.ptr);
   const CUtensorMap *lo = P.has_lo_halo ? &in.tm_lo : &in.tm;
   const CUtensorMap *hi = P.has_hi_halo ? &in.tm_hi : &in.tm;
   stage_stream_kernel<DIMS, R, MODE><<<G, LY::NTHREADS, smem, st>>>(in.tm, *lo, *hi, tm_psi ? *tm_psi : in.tm,
@@ -568,6 +569,10 @@ static nlse2shoc_status launch_stage(nlse2shoc_t H, Field &psi, int s, double dt
   // in L2 when this stage starts (NLSE_NO_REV=1 disables)
   static const bool no_rev = getenv("NLSE_NO_REV") != nullptr;
   P.rev = (!no_rev && (s == 2 || s == 4)) ? 1 : 0;
+  // base pointers of the pointwise streams (must match the maps passed to launch_stream)
+  P.in_P[0] = reinterpret_cast<const cplx<R> *>(psi.ptr);
+  P.in_P[1] = reinterpret_cast<const cplx<R> *>(H->acc.ptr);
+  P.in_P[2] = nullptr;
   Field &in = stage_input(H, psi, s);
   cplx<R> *pPsi = reinterpret_cast<cplx<R> *>(psi.ptr), *pA = reinterpret_cast<cplx<R> *>(H->TA.ptr),
           *pB = reinterpret_cast<cplx<R> *>(H->TB.ptr), *pAcc = reinterpret_cast<cplx<R> *>(H->acc.ptr);
@@ -590,7 +595,11 @@ static nlse2shoc_status launch_stage(nlse2shoc_t H, Field &psi, int s, double dt
       case 4:
         P.cb = R(dt / 6.0); P.out_T = pPsi;
         if constexpr (DIMS >= 2)
+        {
+          P.in_P[1] = reinterpret_cast<const cplx<R> *>(H->TA.ptr);
+          P.in_P[2] = reinterpret_cast<const cplx<R> *>(H->TB.ptr);
           return launch_stream<DIMS, R, M_S4X>(H, in, &psi.tm_pt, &H->TA.tm_pt, P, st, &H->TB.tm_pt);
+        }
         else return launch_line<R, M_S4X>(H, in.ptr, psi.ptr, H->TA.ptr, P, st, H->TB.ptr);
       default:
         break;

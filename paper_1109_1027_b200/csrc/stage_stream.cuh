@@ -29,6 +29,10 @@
 
 #include "common.cuh"
 
+#ifndef NLSE_ROW_BULK
+#define NLSE_ROW_BULK 1
+#endif
+
 namespace nlse {
 
 // Stage kinds.  M_S1..M_S4: the four RK4 stages with the Psi-space accumulator (16 transfers
@@ -202,6 +206,8 @@ template <typename R> struct StageParams {
   int lead;              // max planes a tile's producer may run ahead of its neighbours
   int lead_pair;         // couple only x-partner tiles (t, t^1) instead of all 4 neighbours
   uint32_t *rbar;        // round barrier counter (producers start each round together), or null
+  const cplx<R> *in_T;   // stencil input field (2D rows may be bulk-copied instead of tiled)
+  const cplx<R> *in_P[3];  // pointwise fields (Psi^n, acc / T_A, T_B) for 2D row bulk copies
   cplx<R> *out_T;        // T_s (stages 1-3), psi^{n+1} (stage 4), L (laplacian mode)
   cplx<R> *out_acc;      // accumulator (stages 1-3)
 };
@@ -424,6 +430,10 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
           if (m) {
             mbar_arrive_expect_tx(&fullT[slot], LY::SLOT_BYTES);
             CT *dst = ring + size_t(slot) * LY::SLOT;
+            // 2D interior row segment: one contiguous bulk copy instead of NBOX tensor boxes
+            if (DIMS == 2 && NLSE_ROW_BULK && m == &tm_T && P.in_T && x0 - 2 >= 0 && x0 - 2 + W <= P.nx) {
+              bulk_load_hint(dst, P.in_T + int64_t(pz) * P.pitch + (x0 - 2), LY::SLOT_BYTES, &fullT[slot], pol_keep);
+            } else
 #pragma unroll
             for (int b = 0; b < C::NBOX; ++b) {
               const int c0 = (x0 - 2) * LY::EPC + b * LY::BW;
@@ -450,6 +460,11 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
                                        : LY::template needs_t3<MODE>();
             if (!want) continue;
             const CUtensorMap *m = q == 0 ? &tm_psi : (q == 1 ? &tm_acc : &tm_t3);
+            if (DIMS == 2 && NLSE_ROW_BULK && P.in_P[q] && x0 + TX <= P.nx) {  // whole row segment
+              bulk_load_hint(dst + (q == 0 ? 0 : (q == 1 ? ACC_OFF : T3_OFF)), P.in_P[q] + int64_t(k) * P.pitch + x0,
+                             LY::PTILE_BYTES, &fullP[slot], q == 1 ? pol_acc : pol_stream);
+              continue;
+            }
 #pragma unroll
             for (int b = 0; b < C::NBOXP; ++b) {
               const int c0 = x0 * LY::EPC + b * LY::BWP;
