@@ -469,7 +469,24 @@ static nlse2shoc_status launch_line(nlse2shoc_t H, const void *in, const void *p
 #ifndef NLSE_LINE_PT
 #define NLSE_LINE_PT 1
 #endif
-  if (sizeof(R) == 8 && !NLSE_LINE_TILE_C128) {
+#ifndef NLSE_LINE_STREAM
+#define NLSE_LINE_STREAM 1
+#endif
+  // complex128 grids of >= 16 segments: the persistent bulk-copy ring (C2 0.187 -> 0.152 ms per
+  // step); complex64 keeps the 256-point tiles (0.109 vs 0.113 ms with the ring)
+  if (NLSE_LINE_STREAM && sizeof(R) == 8 && H->nx >= 16 * LineStream<R>::SEG) {
+    static std::atomic<uint64_t> attr{0};
+    const size_t smem = line_stream_smem<R, MODE>();
+    if (attr_needed(attr)) {
+      CUDA_TRY(cudaFuncSetAttribute(line_stream_kernel<R, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      attr_done(attr);
+    }
+    const int64_t nseg = (H->nx + LineStream<R>::SEG - 1) / LineStream<R>::SEG;
+    const int grid = int(std::min<int64_t>(nseg, H->num_sms));
+    line_stream_kernel<R, MODE><<<grid, LineStream<R>::NT, smem, st>>>(
+        reinterpret_cast<const cplx<R> *>(in), reinterpret_cast<const cplx<R> *>(psi),
+        reinterpret_cast<const cplx<R> *>(acc), reinterpret_cast<const cplx<R> *>(t3), P);
+  } else if (sizeof(R) == 8 && !NLSE_LINE_TILE_C128) {
     const int64_t blocks = std::min<int64_t>((H->nx + threads - 1) / threads, int64_t(H->num_sms) * 8);
     stage_line_kernel<R, MODE><<<int(blocks), threads, 0, st>>>(
         reinterpret_cast<const cplx<R> *>(in), reinterpret_cast<const cplx<R> *>(psi),

@@ -164,6 +164,127 @@ __global__ void __launch_bounds__(256) line_tile_kernel(const cplx<R> *__restric
   }
 }
 
+// Persistent 1D stage: each CTA walks segments of SEG points; one thread prefetches the next
+// NS-1 segments (stencil input with a 4-point halo, and the pointwise streams) into a ring of
+// shared-memory slots with one contiguous cp.async.bulk per stream, so the whole CTA computes
+// from shared memory while the following segments stream in.  Segments touching either end of
+// the grid are loaded with plain loads (out-of-range halo entries are never read: the two
+// points at each end go through line_point on global memory).  Same arithmetic as
+// line_tile_kernel.
+template <typename R> struct LineStream {
+  static constexpr int SEG = 1024, NS = sizeof(R) == 4 ? 4 : 3, NT = 256;
+};
+template <typename R, int MODE> __host__ __device__ constexpr int line_npa() {
+  return MODE == M_S4X ? 3 : ((MODE == M_S4R || MODE == M_S2 || MODE == M_S3 || MODE == M_S4) ? 2 :
+                              ((MODE == M_S2R || MODE == M_S3R) ? 1 : 0));
+}
+template <typename R, int MODE> __host__ __device__ constexpr size_t line_stream_smem() {
+  using LS = LineStream<R>;
+  return size_t(LS::NS) * ((LS::SEG + 8) + size_t(line_npa<R, MODE>()) * LS::SEG) * sizeof(cplx<R>) + 8 * LS::NS;
+}
+
+template <typename R, int MODE>
+__global__ void __launch_bounds__(256, 1) line_stream_kernel(const cplx<R> *__restrict__ Tin, const cplx<R> *__restrict__ psi,
+                                                             const cplx<R> *__restrict__ acc, const cplx<R> *__restrict__ t3,
+                                                             const StageParams<R> P) {
+  using CT = cplx<R>;
+  using LS = LineStream<R>;
+  constexpr int SEG = LS::SEG, NS = LS::NS, NPA = line_npa<R, MODE>();
+  constexpr int SLOT = (SEG + 8) + NPA * SEG;  // complex per ring stage: T (+halo), then the P streams
+  extern __shared__ __align__(1024) unsigned char lsm[];
+  CT *ring = reinterpret_cast<CT *>(lsm);
+  uint64_t *full = reinterpret_cast<uint64_t *>(lsm + size_t(NS) * SLOT * sizeof(CT));
+  const int n = P.nx;
+  const int nseg = (n + SEG - 1) / SEG;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const CT *pstream[3] = {psi, acc, t3};
+  auto seg_of = [&](int j) { const int sg = blockIdx.x + j * gridDim.x; return P.rev ? nseg - 1 - sg : sg; };
+  auto interior = [&](int sg) { return int64_t(sg) * SEG - 4 >= 0 && int64_t(sg + 1) * SEG + 4 <= n; };
+  auto issue = [&](int j) {  // thread 0: prefetch segment j into ring stage j % NS
+    const int sg = seg_of(j);
+    uint64_t *bar = &full[j % NS];
+    if (!interior(sg)) {
+      mbar_arrive(bar);  // loaded by the whole CTA after the wait
+      return;
+    }
+    CT *slot = ring + size_t(j % NS) * SLOT;
+    const uint32_t tb = uint32_t((SEG + 8) * sizeof(CT)), pb = uint32_t(SEG * sizeof(CT));
+    mbar_arrive_expect_tx(bar, tb + NPA * pb);
+    const uint64_t pol = policy_evict_normal();
+    bulk_load_hint(slot, Tin + int64_t(sg) * SEG - 4, tb, bar, pol);
+#pragma unroll
+    for (int q = 0; q < NPA; ++q) bulk_load_hint(slot + (SEG + 8) + q * SEG, pstream[q] + int64_t(sg) * SEG, pb, bar, pol);
+  };
+  const int njobs = blockIdx.x < nseg ? (nseg - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  if (threadIdx.x == 0)
+    for (int j = 0; j < NS - 1 && j < njobs; ++j) issue(j);
+  for (int j = 0; j < njobs; ++j) {
+    if (threadIdx.x == 0 && j + NS - 1 < njobs) issue(j + NS - 1);
+    const int sg = seg_of(j);
+    CT *slot = ring + size_t(j % NS) * SLOT;
+    mbar_wait(&full[j % NS], (j / NS) & 1);
+    const int64_t t0 = int64_t(sg) * SEG;
+    if (!interior(sg)) {  // grid-end segment: plain loads, halo entries outside the grid zeroed
+      for (int k = threadIdx.x; k < SEG + 8; k += LS::NT) {
+        const int64_t g = t0 - 4 + k;
+        slot[k] = (g >= 0 && g < n) ? Tin[g] : mk<R>(R(0), R(0));
+      }
+      for (int q = 0; q < NPA; ++q)
+        for (int k = threadIdx.x; k < SEG; k += LS::NT) {
+          const int64_t g = t0 + k;
+          slot[(SEG + 8) + q * SEG + k] = g < n ? pstream[q][g] : mk<R>(R(0), R(0));
+        }
+      __syncthreads();
+    }
+    const CT *sT = slot, *sP = slot + (SEG + 8);
+#pragma unroll
+    for (int q = 0; q < SEG / LS::NT; ++q) {
+      const int kk = q * LS::NT + threadIdx.x;
+      const int64_t i = t0 + kk;
+      if (i >= n) break;
+      CT c, L, t;
+      if (i < 2 || i >= n - 2) {
+        t = line_point(Tin, i, n, P, c, L);
+      } else {
+        const CT *pp = sT + kk + 4;
+        c = pp[0];
+        L = axpy(axpy((-P.c30) * c, P.c1x, pp[-1] + pp[1]), -P.cx, pp[-2] + pp[2]);
+        const R N = fma(P.s, norm2(c), -potential(P, int(i), 0, 0));
+        t = axpy(N * c, P.a, L);
+      }
+      const CT ps = NPA > 0 ? sP[kk] : c, a1 = NPA > 1 ? sP[SEG + kk] : c, a2 = NPA > 2 ? sP[2 * SEG + kk] : c;
+      if (MODE == M_LAP) {
+        P.out_T[i] = L;
+      } else if (MODE == M_S1R) {
+        P.out_T[i] = iaxpy(c, P.cb, t);
+      } else if (MODE == M_S2R) {
+        P.out_acc[i] = iaxpy(axpy(ps, R(1.0 / 3.0), c - ps), P.ca, t);
+        P.out_T[i] = iaxpy(ps, P.cb, t);
+      } else if (MODE == M_S3R) {
+        P.out_T[i] = iaxpy(ps, P.cb, t);
+      } else if (MODE == M_S4R) {
+        P.out_T[i] = iaxpy(axpy(a1, R(1.0 / 3.0), c - ps), P.cb, t);
+      } else if (MODE == M_S4X) {
+        const CT dsum = axpy(a1 - ps, R(2), a2 - ps) + (c - ps);
+        P.out_T[i] = iaxpy(axpy(ps, R(1.0 / 3.0), dsum), P.cb, t);
+      } else if (MODE == M_S1) {
+        P.out_acc[i] = iaxpy(c, P.ca, t);
+        P.out_T[i] = iaxpy(c, P.cb, t);
+      } else if (MODE == M_S2 || MODE == M_S3) {
+        P.out_acc[i] = iaxpy(a1, P.ca, t);
+        P.out_T[i] = iaxpy(ps, P.cb, t);
+      } else {  // M_S4
+        P.out_T[i] = iaxpy(a1, P.cb, t);
+      }
+    }
+    __syncthreads();  // every thread is done with this ring stage before it is refilled
+  }
+}
+
 // Resident small-grid 1D solver: the whole grid (Psi, T_A, T_B, acc) lives in one CTA's
 // shared memory and the CTA runs all nsteps x 4 stages of an nlse2shoc_rk4 call, separated
 // by barriers.  Same per-point arithmetic as stage_line_kernel; one launch per call instead

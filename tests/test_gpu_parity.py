@@ -337,3 +337,37 @@ def test_fig1_on_gpu():
     printed = {0.25: 3.9355, 0.125: 3.9788, 0.0625: 3.9941, 0.03125: 3.9984}
     for h2, o in printed.items():
         assert abs(metrics.order(E[2 * h2][0], E[h2][0], 2 * h2, h2) - o) < 5e-3
+
+
+@pytest.mark.parametrize("variant", [0, 2, 6])
+@pytest.mark.parametrize("bc,V,dtype", [("dirichlet", "harmonic", "c128"), ("lapzero", "array", "c128"),
+                                        ("dirichlet", "none", "c64"), ("lapzero", "harmonic", "c128")])
+def test_1d_stream_kernel_parity(bc, V, dtype, variant):
+    """1D grids of >= 16 segments run the persistent bulk-copy kernel (line_stream_kernel):
+    a ragged 40 003-point grid, 10 steps, against the oracle."""
+    w = _small(1, (40003,), bc, dtype, V)
+    S = H.gpu_solver(w, dtype, variant)
+    psi = H.psi0_host(w, dtype)
+    P = H.oracle_problem(w)
+    dt = 0.8 * oracle.kmax(P, psi.astype(np.complex128))
+    g = _dev(psi)
+    S.rk4(g, dt, 10)
+    ref = oracle.rk4(P, psi.astype(np.complex128), dt, 10)
+    assert H.rel_l2(g.cpu().numpy(), ref) <= H.TOL[dtype]
+    L = S.laplacian(_dev(psi)).cpu().numpy()
+    assert H.rel_l2(L, oracle.laplacian(P, psi.astype(np.complex128))) <= (1e-12 if dtype == "c128" else 1e-5)
+
+
+def test_1d_stream_kernel_msd():
+    """MSD boundary through the persistent 1D kernel (Exp. 1 geometry at h = 1/512)."""
+    w = configs.EXP_DARK(1.0 / 512)
+    assert w["grid"]["n"][0] >= 16 * 1024
+    psi = H.psi0_host(w, "c128")
+    P = H.oracle_problem(w)
+    S = H.gpu_solver(w, "c128")
+    dt = 0.5 * oracle.kmax(P, psi)  # h = 1/512 is far inside Exp. 1's k = 5e-4 stability limit
+    g = _dev(psi)
+    S.rk4(g, dt, 20)
+    ref = oracle.rk4(P, psi, dt, 20)
+    assert np.isfinite(ref).all()
+    assert H.rel_l2(g.cpu().numpy(), ref) <= 1e-12
