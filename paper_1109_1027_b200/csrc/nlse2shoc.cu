@@ -474,7 +474,10 @@ static nlse2shoc_status launch_line(nlse2shoc_t H, const void *in, const void *p
 #endif
   // complex128 grids of >= 16 segments: the persistent bulk-copy ring (C2 0.187 -> 0.152 ms per
   // step); complex64 keeps the 256-point tiles (0.109 vs 0.113 ms with the ring)
-  if (NLSE_LINE_STREAM && sizeof(R) == 8 && H->nx >= 16 * LineStream<R>::SEG) {
+#ifndef NLSE_LINE_STREAM64
+#define NLSE_LINE_STREAM64 0
+#endif
+  if (NLSE_LINE_STREAM && (sizeof(R) == 8 || NLSE_LINE_STREAM64) && H->nx >= 16 * LineStream<R>::SEG) {
     static std::atomic<uint64_t> attr{0};
     const size_t smem = line_stream_smem<R, MODE>();
     if (attr_needed(attr)) {
