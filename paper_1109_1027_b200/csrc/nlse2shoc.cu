@@ -86,6 +86,7 @@ struct nlse2shoc_s {
   int rng_b = 0, rng_e = 0;  // plane range of the next stage launch (0, 0: the whole slab)
   int reserve_sms = 0;       // SMs left free for a concurrent NCCL exchange (interior launches)
   cudaStream_t comm_st = nullptr;  // edge-first halo exchange: side stream + events
+  cudaStream_t cap_st = nullptr;   // private stream for CUDA-graph capture
   cudaEvent_t ev_edge = nullptr, ev_recv = nullptr;
   nlse2shoc_alloc_fn alloc = nullptr;  // device allocator captured at create (null: cudaMalloc)
   nlse2shoc_free_fn dfree = nullptr;
@@ -783,6 +784,40 @@ static nlse2shoc_status run_rk4_overlapped(View &v, double dt, int64_t nsteps, c
   return NLSE2SHOC_OK;
 }
 
+// Single-slab calls of >= 4 steps: the four stage launches of one step are captured once
+// into a CUDA graph (on a private stream) and the graph is replayed nsteps times on the
+// caller's stream, which trims per-launch overhead on small grids (NLSE_NO_GRAPH=1: off).
+static bool graph_ok() {
+  static const bool off = getenv("NLSE_NO_GRAPH") != nullptr;
+  return !off;
+}
+
+static nlse2shoc_status run_rk4_graph(View &v, double dt, int64_t nsteps, cudaStream_t st) {
+  nlse2shoc_t H = v.hs[0];
+  if (!H->cap_st) CUDA_TRY(cudaStreamCreateWithFlags(&H->cap_st, cudaStreamNonBlocking));
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  CUDA_TRY(cudaStreamBeginCapture(H->cap_st, cudaStreamCaptureModeRelaxed));
+  nlse2shoc_status r = NLSE2SHOC_OK;
+  for (int s = 1; s <= 4 && r == NLSE2SHOC_OK; ++s) r = stage(H, v.psis[0], s, dt, nullptr, H->cap_st);
+  const cudaError_t ec = cudaStreamEndCapture(H->cap_st, &graph);
+  if (r != NLSE2SHOC_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return r;
+  }
+  if (ec != cudaSuccess) return fail(NLSE2SHOC_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ec));
+  const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ei != cudaSuccess) return fail(NLSE2SHOC_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei));
+  const int64_t per_step = H->launches;
+  cudaError_t el = cudaSuccess;
+  for (int64_t n = 0; n < nsteps && el == cudaSuccess; ++n) el = cudaGraphLaunch(exec, st);
+  cudaGraphExecDestroy(exec);  // deferred by the driver until the launches complete
+  if (el != cudaSuccess) return fail(NLSE2SHOC_ECUDA, std::string("graph launch: ") + cudaGetErrorString(el));
+  H->launches = per_step * nsteps;
+  return NLSE2SHOC_OK;
+}
+
 static nlse2shoc_status run_rk4(View &v, double dt, int64_t nsteps, cudaStream_t st) {
   if (v.hs.size() == 1 && v.hs[0]->variant == 4) return rk4_pairs(v.hs[0], v.psis[0], dt, nsteps, st);
   if (v.hs.size() == 1 && resident_ok(v.hs[0])) {
@@ -791,6 +826,7 @@ static nlse2shoc_status run_rk4(View &v, double dt, int64_t nsteps, cudaStream_t
                                      : rk4_resident_1d<double>(H, v.psis[0], dt, nsteps, st);
   }
   if (overlap_ok(v)) return run_rk4_overlapped(v, dt, nsteps, st);
+  if (v.hs.size() == 1 && !v.hs[0]->sharded && nsteps >= 4 && graph_ok()) return run_rk4_graph(v, dt, nsteps, st);
   for (int64_t n = 0; n < nsteps; ++n)
     for (int s = 1; s <= 4; ++s) {
       TRY(exchange(v, s, st));
@@ -1363,6 +1399,7 @@ void nlse2shoc_destroy(nlse2shoc_t H) {
   if (H->ev_edge) cudaEventDestroy(H->ev_edge);
   if (H->ev_recv) cudaEventDestroy(H->ev_recv);
   if (H->comm_st) cudaStreamDestroy(H->comm_st);
+  if (H->cap_st) cudaStreamDestroy(H->cap_st);
 #ifdef NLSE_WITH_NCCL
   if (H->comm) ncclCommDestroy(H->comm);
 #endif
