@@ -108,10 +108,6 @@ struct nlse2shoc_s {
   size_t bytes = 0;
   int num_sms = 148;
   int64_t launches = 0;
-  uint32_t *prog = nullptr;  // per-tile progress words of the stage kernel (neighbour coupling)
-  int prog_cap = 0;
-  uint32_t epoch = 0;
-  uint32_t *rbar = nullptr;  // round-barrier counter of the stage kernel
   // loopback (single-GPU emulation of z-slab sharding, SURVEY §4 T3'): virtual slabs that
   // exchange halos by device copies instead of NCCL; empty for ordinary handles
   std::vector<nlse2shoc_s *> slabs;
@@ -353,29 +349,6 @@ static nlse2shoc_status launch_stream(nlse2shoc_t H, Field &in, const CUtensorMa
   P.nchunk = best;
   P.ntiles = ncol * best;
   const int G = std::min(G0, P.ntiles);
-  // neighbour coupling (NLSE_LEAD=0 disables): per-tile progress words, epoch-tagged
-  static const int lead = getenv("NLSE_LEAD") ? atoi(getenv("NLSE_LEAD")) : 0;
-  static const int rbar = getenv("NLSE_RBAR") ? atoi(getenv("NLSE_RBAR")) : 0;
-  if (lead > 0 || rbar) P.rev = 0;  // the coupling experiments index neighbours in forward order
-  if (rbar && P.ntiles > G) {
-    if (!H->rbar) CUDA_TRY(dev_malloc(H, &H->rbar, 256));
-    CUDA_TRY(cudaMemsetAsync(H->rbar, 0, sizeof(uint32_t), st));
-    P.rbar = H->rbar;
-  }
-  if (lead > 0) {
-    if (H->prog_cap < P.ntiles) {
-      if (H->prog) dev_free(H, H->prog);
-      CUDA_TRY(dev_malloc(H, &H->prog, sizeof(uint32_t) * P.ntiles));
-      CUDA_TRY(cudaMemsetAsync(H->prog, 0, sizeof(uint32_t) * P.ntiles, st));
-      H->prog_cap = P.ntiles;
-    }
-    H->epoch = (H->epoch + 1) & 0xffff;
-    P.prog = H->prog;
-    P.epoch = H->epoch;
-    P.lead = lead;
-    static const int pair = getenv("NLSE_LEAD_PAIR") ? atoi(getenv("NLSE_LEAD_PAIR")) : 1;
-    P.lead_pair = pair;
-  }
   P.in_T = reinterpret_cast<const cplx<R> *>(in.ptr);
   const CUtensorMap *lo = P.has_lo_halo ? &in.tm_lo : &in.tm;
   const CUtensorMap *hi = P.has_hi_halo ? &in.tm_hi : &in.tm;
@@ -1393,8 +1366,6 @@ void nlse2shoc_destroy(nlse2shoc_t H) {
     if (f->halo_hi) dev_free(H, f->halo_hi);
   }
   if (H->vtab) dev_free(H, H->vtab);
-  if (H->prog) dev_free(H, H->prog);
-  if (H->rbar) dev_free(H, H->rbar);
   if (H->red) dev_free(H, H->red);
   if (H->ev_edge) cudaEventDestroy(H->ev_edge);
   if (H->ev_recv) cudaEventDestroy(H->ev_recv);

@@ -201,11 +201,6 @@ template <typename R> struct StageParams {
   int vkind;             // 0 none, 1 harmonic tables, 2 array
   const R *vx, *vy, *vz; // harmonic tables (vz indexed by GLOBAL streamed index)
   const R *varr;         // array potential (local slab, row pitch nx)
-  uint32_t *prog;        // per-tile producer progress (epoch << 16 | planes issued), or null
-  uint32_t epoch;        // launch tag of this stage's progress words
-  int lead;              // max planes a tile's producer may run ahead of its neighbours
-  int lead_pair;         // couple only x-partner tiles (t, t^1) instead of all 4 neighbours
-  uint32_t *rbar;        // round barrier counter (producers start each round together), or null
   const cplx<R> *in_T;   // stencil input field (2D rows may be bulk-copied instead of tiled)
   const cplx<R> *in_P[3];  // pointwise fields (Psi^n, acc / T_A, T_B) for 2D row bulk copies
   cplx<R> *out_T;        // T_s (stages 1-3), psi^{n+1} (stage 4), L (laplacian mode)
@@ -381,47 +376,9 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
         const int chunk = tt / ncol, col = tt % ncol;
         const int x0 = (col % P.ncx) * TX, y0 = (col / P.ncx) * TY;
         const int kb = P.zb + chunk * chunk_len, ke = min(P.ze, kb + chunk_len);
-        // Round barrier: every producer starts round r only after all producers finished
-        // issuing round r-1, so the tiles of a round stream the same planes at the same time
-        // and a tile's halo rows/columns are L2 hits when its neighbours load them.
-        if (P.rbar && t >= G) {
-          const uint32_t need = uint32_t(t / G) * uint32_t(G);
-          while (ld_relaxed_gpu(P.rbar) < need) __nanosleep(64);
-        }
-        // Neighbour coupling: tiles that share halo data with this one and run in the same
-        // round keep their producers within `lead` planes of each other, so one tile's halo
-        // rows/columns are still in L2 when its neighbour streams the same plane.
-        int nb[4], nnb = 0;
-        if (P.prog) {
-          const int round = t / G, cx = col % P.ncx, cyy = col / P.ncx;
-          if (P.lead_pair) {  // only the x-partner tile (t ^ 1), run by CTA blockIdx ^ 1
-            const int pt = t ^ 1;
-            if (pt < P.ntiles && pt / G == round && (pt % ncol) / P.ncx == cyy) nb[nnb++] = pt;
-          } else {
-            const int cand[4] = {cx > 0 ? t - 1 : -1, cx + 1 < P.ncx ? t + 1 : -1, cyy > 0 ? t - P.ncx : -1,
-                                 cyy + 1 < P.ncy ? t + P.ncx : -1};
-            for (int i = 0; i < 4; ++i)
-              if (cand[i] >= 0 && cand[i] < P.ntiles && cand[i] / G == round) nb[nnb++] = cand[i];
-          }
-        }
-        int issued = 0, seen = 0;  // planes issued for this tile; min neighbour progress seen
-        auto gate = [&](int j) {
-          if (nnb == 0 || j - P.lead <= seen) return;
-          for (int spin = 0; spin < 4000; ++spin) {
-            int m = 1 << 30;
-            for (int i = 0; i < nnb; ++i) {
-              const uint32_t v = ld_relaxed_gpu(P.prog + nb[i]);
-              m = min(m, (v >> 16) == P.epoch ? int(v & 0xffff) : 0);
-            }
-            seen = m;
-            if (j - P.lead <= seen) return;
-            __nanosleep(100);
-          }
-        };
         auto produceT = [&](int p) {
           const uint32_t slot = tcnt % RT, par = (tcnt / RT) & 1;
           mbar_wait_backoff(&emptyT[slot], par ^ 1);
-          gate(issued);
           const CUtensorMap *m = nullptr;
           int pz = p;
           if (p >= 0 && p < P.nz) m = &tm_T;
@@ -445,8 +402,6 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
             mbar_arrive(&fullT[slot]);
           }
           ++tcnt;
-          ++issued;
-          if (P.prog) st_relaxed_gpu(P.prog + t, (P.epoch << 16) | uint32_t(issued));
         };
         auto produceP = [&](int k) {
           const uint32_t slot = pcnt % RPM, par = (pcnt / RPM) & 1;
@@ -482,7 +437,6 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
           produceT(k + 2);
           if (NPA) produceP(k);
         }
-        if (P.rbar) atomicAdd(P.rbar, 1u);
       }
     }
     return;
