@@ -251,17 +251,14 @@ template <typename R> static void fill_params(nlse2shoc_t H, StageParams<R> &P) 
   // physical spacing of kernel axes: x = axis 0; y = axis 1 (3D); streamed = axis dims-1
   const double hx = H->h[0], hy = H->dims == 3 ? H->h[1] : 1.0, hz = H->dims >= 2 ? H->h[H->dims - 1] : 1.0;
   const double hh[3] = {hx * hx, hy * hy, hz * hz};
-  const bool has[3] = {true, H->dims == 3, H->dims >= 2};
-  double w0 = 0.0, w1[3], w2[3];
+  double w1[3], w2[3];
   for (int d = 0; d < 3; ++d) {
     if (H->scheme == NLSE2SHOC_SCHEME_CD) {  // `uttmp`: delta^2 per axis
       w1[d] = 1.0 / hh[d];
       w2[d] = 0.0;
-      if (has[d]) w0 += 2.0 / hh[d];
     } else {  // 5-point wide form of the two-step scheme: (16, -1, -30)/(12 h^2)
       w1[d] = 16.0 / (12.0 * hh[d]);
       w2[d] = 1.0 / (12.0 * hh[d]);
-      if (has[d]) w0 += 30.0 / (12.0 * hh[d]);
     }
   }
   P.cx = R(w2[0]);
@@ -270,7 +267,6 @@ template <typename R> static void fill_params(nlse2shoc_t H, StageParams<R> &P) 
   P.c1x = R(w1[0]);
   P.c1y = R(w1[1]);
   P.c1z = R(w1[2]);
-  P.c30 = R(w0);
   P.ihx2 = R(1.0 / (hx * hx));
   P.ihy2 = R(1.0 / (hy * hy));
   P.ihz2 = R(1.0 / (hz * hz));

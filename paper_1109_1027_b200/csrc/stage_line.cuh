@@ -42,7 +42,7 @@ __device__ __forceinline__ cplx<R> line_interior(const cplx<R> *__restrict__ Tin
   else m2 = axpy(R(2) * m1 - c, P.hx2, line_lambda<R, MSD>(Tin, 0, n, P));
   if (i <= n - 3) p2 = Tin[i + 2];
   else p2 = axpy(R(2) * p1 - c, P.hx2, line_lambda<R, MSD>(Tin, n - 1, n, P));
-  L = axpy(axpy((-P.c30) * c, P.c1x, m1 + p1), -P.cx, m2 + p2);  // 2SHOC wide form, or CD (cx = 0)
+  L = lap5(R(2) * c, P.c1x, P.cx, m1, p1, m2, p2);  // 2SHOC wide form, or CD (cx = 0)
   const R N = fma(P.s, norm2(c), -potential(P, int(i), 0, 0));
   return axpy(N * c, P.a, L);  // a L + N c
 }
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(256) line_tile_kernel(const cplx<R> *__restric
     } else {
       const CT *pp = sT + (i - t0 + 4);
       c = pp[0];
-      L = axpy(axpy((-P.c30) * c, P.c1x, pp[-1] + pp[1]), -P.cx, pp[-2] + pp[2]);
+      L = lap5(R(2) * c, P.c1x, P.cx, pp[-1], pp[1], pp[-2], pp[2]);
       const R N = fma(P.s, norm2(c), -potential(P, int(i), 0, 0));
       t = axpy(N * c, P.a, L);
     }
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(256, 1) line_stream_kernel(const cplx<R> *__re
       } else {
         const CT *pp = sT + kk + 4;
         c = pp[0];
-        L = axpy(axpy((-P.c30) * c, P.c1x, pp[-1] + pp[1]), -P.cx, pp[-2] + pp[2]);
+        L = lap5(R(2) * c, P.c1x, P.cx, pp[-1], pp[1], pp[-2], pp[2]);
         const R N = fma(P.s, norm2(c), -potential(P, int(i), 0, 0));
         t = axpy(N * c, P.a, L);
       }

@@ -249,7 +249,7 @@ __global__ void NLSE_PAIR_BOUNDS(PLayout<DIMS, R>::NTHREADS)
   const int cg = ct % CPT, rg = ct / CPT;
   const int lx0 = cg * PPX, ly0 = rg * RPW;  // phase-B points of this thread (tile-relative)
   const CT zero = mk<R>(R(0), R(0));
-  const R cx = P.cx, cy = P.cy, cz = P.cz, c30 = P.c30, pa_ = P.a, ps_ = P.s;
+  const R cx = P.cx, cy = P.cy, cz = P.cz, pa_ = P.a, ps_ = P.s;
   const R c16x = P.c1x, c16y = P.c1y, c16z = P.c1z, cA = P.cA, ca = P.ca, cb = P.cb;
   const int nx = P.nx, ny = P.ny, nz = P.nz, NZ = P.NZ, z0 = P.z0;
   uint32_t icnt = 0, scnt = 0, acnt = 0, mcnt = 0;
@@ -445,15 +445,9 @@ __global__ void NLSE_PAIR_BOUNDS(PLayout<DIMS, R>::NTHREADS)
 #pragma unroll
           for (int q = 0; q < PPX; ++q) {
             const CT c = run[q + 2];
-            CT L = (-c30) * c;
-            L = axpy(L, c16x, run[q + 1] + run[q + 3]);
-            L = axpy(L, -cx, run[q] + run[q + 4]);
-            L = axpy(L, c16z, zm1[q] + zp1[q]);
-            L = axpy(L, -cz, zm2[q] + zp2[q]);
-            if (DIMS == 3) {
-              L = axpy(L, c16y, ym1[q] + yp1[q]);
-              L = axpy(L, -cy, ym2[q] + yp2[q]);
-            }
+            // sum_d (16 (g-1 + g+1 - 2 g0) - (g-2 + g+2 - 2 g0)) / (12 h_d^2)
+            CT L = lap_wide<DIMS>(c, c16x, cx, c16y, cy, c16z, cz, run[q + 1], run[q + 3], run[q], run[q + 4],
+                                 ym1[q], yp1[q], ym2[q], yp2[q], zm1[q], zp1[q], zm2[q], zp2[q]);
             const R N = fma(ps_, norm2(c), -(a_v[i][q] + vzj));
             const CT tF = axpy(N * c, pa_, L);
             out[q] = B ? iaxpy(psv[q], cA, tF) : iaxpy(c, cA, tF);
@@ -492,15 +486,9 @@ __global__ void NLSE_PAIR_BOUNDS(PLayout<DIMS, R>::NTHREADS)
           for (int q = 0; q < PPX; ++q) {
             const int gx = x0 + lx + q;
             const CT c = run[q + 2];
-            CT L = (-c30) * c;
-            L = axpy(L, c16x, run[q + 1] + run[q + 3]);
-            L = axpy(L, -cx, run[q] + run[q + 4]);
-            L = axpy(L, c16z, zm1[q] + zp1[q]);
-            L = axpy(L, -cz, zm2[q] + zp2[q]);
-            if (DIMS == 3) {
-              L = axpy(L, c16y, ym1[q] + yp1[q]);
-              L = axpy(L, -cy, ym2[q] + yp2[q]);
-            }
+            // sum_d (16 (g-1 + g+1 - 2 g0) - (g-2 + g+2 - 2 g0)) / (12 h_d^2)
+            CT L = lap_wide<DIMS>(c, c16x, cx, c16y, cy, c16z, cz, run[q + 1], run[q + 3], run[q], run[q + 4],
+                                 ym1[q], yp1[q], ym2[q], yp2[q], zm1[q], zp1[q], zm2[q], zp2[q]);
             const bool valid = gx >= 0 && gx < nx;
             R V = R(0);
             if (valid) {
@@ -607,15 +595,9 @@ __global__ void NLSE_PAIR_BOUNDS(PLayout<DIMS, R>::NTHREADS)
           for (int q = 0; q < PPX; ++q) {
             const int gx = x0 + lx0 + q;
             const CT c = run[q + 2];
-            CT L = (-c30) * c;
-            L = axpy(L, c16x, run[q + 1] + run[q + 3]);
-            L = axpy(L, -cx, run[q] + run[q + 4]);
-            L = axpy(L, c16z, qm1[r][q] + qp1[r][q]);
-            L = axpy(L, -cz, qm2[r][q] + zp2[q]);
-            if (DIMS == 3) {
-              L = axpy(L, c16y, ym1[q] + yp1[q]);
-              L = axpy(L, -cy, ym2[q] + yp2[q]);
-            }
+            // sum_d (16 (g-1 + g+1 - 2 g0) - (g-2 + g+2 - 2 g0)) / (12 h_d^2)
+            CT L = lap_wide<DIMS>(c, c16x, cx, c16y, cy, c16z, cz, run[q + 1], run[q + 3], run[q], run[q + 4],
+                                 ym1[q], yp1[q], ym2[q], yp2[q], qm1[r][q], qp1[r][q], qm2[r][q], zp2[q]);
             valid[q] = LEAN || (gx < nx && gy < ny);
             R V;
             if (!LEAN && P.vkind == 2) V = valid[q] ? potential(P, gx, gy, k) : R(0);

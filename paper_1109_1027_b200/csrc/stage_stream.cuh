@@ -189,7 +189,6 @@ template <typename R> struct StageParams {
   int64_t plane;         // elements per plane = pitch * ny
   R cx, cy, cz;          // weight of the +-2 neighbours per axis: 1/(12 h^2) (2SHOC), 0 (CD)
   R c1x, c1y, c1z;       // weight of the +-1 neighbours: 16/(12 h^2) (2SHOC), 1/h^2 (CD)
-  R c30;                 // centre weight of the summed stencil: 30 sum cx (2SHOC), 2 sum 1/h^2 (CD)
   R ihx2, ihy2, ihz2;    // 1/h^2 per axis (delta^2 in the face rule)
   R hx2, hy2, hz2;       // h^2 per axis (ghost formula)
   R a, s, inv_a;
@@ -274,6 +273,35 @@ template <typename R> __device__ __forceinline__ cplx<R> lambda_b(const StagePar
 
 template <typename R> __device__ __forceinline__ cplx<R> d2(cplx<R> m, cplx<R> c, cplx<R> p, R ih2) {
   return ih2 * ((m + p) - R(2) * c);
+}
+
+// One axis of the 5-point wide form (16 (g-1 + g+1 - 2 g0) - (g-2 + g+2 - 2 g0)) / (12 h^2),
+// written with the centre subtracted inside each bracket (c2 = 2 g0) rather than as a separate
+// -30 g0 term: with weights rounded to R the separate form leaves a bias (sum of rounded weights
+// != 0, about eps * 30/(12 h^2) per unit field) that acts as a constant shift of the frequency
+// and grows linearly with the step count in complex64 (C2 500 steps: 5.8e-5 vs the fp64 oracle).
+// (g-1 + g+1) - 2 g0 is exact for slowly varying fields (Sterbenz), so a constant field gives
+// L = 0 exactly and the rounding error scales with the differences, not with the field.
+template <typename R>
+__device__ __forceinline__ cplx<R> lap5(cplx<R> c2, R w16, R w1, cplx<R> m1, cplx<R> p1, cplx<R> m2, cplx<R> p2) {
+  return axpy(w16 * ((m1 + p1) - c2), -w1, (m2 + p2) - c2);
+}
+template <typename R>
+__device__ __forceinline__ cplx<R> lap5(cplx<R> L, cplx<R> c2, R w16, R w1, cplx<R> m1, cplx<R> p1, cplx<R> m2,
+                                        cplx<R> p2) {
+  return axpy(axpy(L, w16, (m1 + p1) - c2), -w1, (m2 + p2) - c2);
+}
+// The 2D/3D stencil: lap5 per axis (x, streamed axis, then y in 3D).
+template <int DIMS, typename R>
+__device__ __forceinline__ cplx<R> lap_wide(cplx<R> c, R w16x, R w1x, R w16y, R w1y, R w16z, R w1z, cplx<R> xm1,
+                                            cplx<R> xp1, cplx<R> xm2, cplx<R> xp2, cplx<R> ym1, cplx<R> yp1,
+                                            cplx<R> ym2, cplx<R> yp2, cplx<R> zm1, cplx<R> zp1, cplx<R> zm2,
+                                            cplx<R> zp2) {
+  const cplx<R> c2 = R(2) * c;
+  cplx<R> L = lap5(c2, w16x, w1x, xm1, xp1, xm2, xp2);
+  L = lap5(L, c2, w16z, w1z, zm1, zp1, zm2, zp2);
+  if (DIMS == 3) L = lap5(L, c2, w16y, w1y, ym1, yp1, ym2, yp2);
+  return L;
 }
 
 // Shared-memory 128-bit helpers: CPV complex values per 16-byte vector.
@@ -454,7 +482,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
   const int lx0 = cg * PPX;                        // first local x of this thread
   const int ly0 = rg * RPW;                        // first local row of this thread
   const CT zero = mk<R>(R(0), R(0));
-  const R cx = P.cx, cy = P.cy, cz = P.cz, c30 = P.c30, pa_ = P.a, ps_ = P.s, ca = P.ca, cb = P.cb;
+  const R cx = P.cx, cy = P.cy, cz = P.cz, pa_ = P.a, ps_ = P.s, ca = P.ca, cb = P.cb;
   const R c16x = P.c1x, c16y = P.c1y, c16z = P.c1z;
   const int nx = P.nx, ny = P.ny, nz = P.nz, NZ = P.NZ, z0 = P.z0;
   uint32_t tcnt = 0, pcnt = 0;
@@ -638,16 +666,9 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
         for (int q = 0; q < PPX; ++q) {
           const int gx = x0 + lx0 + q;
           const CT c = run[q + 2];
-          // 5-point wide form per axis: sum_d (16 (g-1 + g+1) - (g-2 + g+2) - 30 g0) / (12 h_d^2)
-          CT L = (-c30) * c;
-          L = axpy(L, c16x, run[q + 1] + run[q + 3]);
-          L = axpy(L, -cx, run[q] + run[q + 4]);
-          L = axpy(L, c16z, qm1[r][q] + qp1[r][q]);
-          L = axpy(L, -cz, qm2[r][q] + zp2[q]);
-          if (DIMS == 3) {
-            L = axpy(L, c16y, ym1[q] + yp1[q]);
-            L = axpy(L, -cy, ym2[q] + yp2[q]);
-          }
+          // sum_d (16 (g-1 + g+1 - 2 g0) - (g-2 + g+2 - 2 g0)) / (12 h_d^2)
+          CT L = lap_wide<DIMS>(c, c16x, cx, c16y, cy, c16z, cz, run[q + 1], run[q + 3], run[q], run[q + 4],
+                               ym1[q], yp1[q], ym2[q], yp2[q], qm1[r][q], qp1[r][q], qm2[r][q], zp2[q]);
           R V;
           if (P.vkind == 2) V = (gx < nx && gy < ny) ? potential(P, gx, gy, k) : R(0);
           else V = (vxr[q] + vyr[r]) + vzk;
@@ -783,15 +804,9 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
 #pragma unroll
         for (int q = 0; q < PPX; ++q) {
           const CT c = run[q + 2];
-          CT L = (-c30) * c;
-          L = axpy(L, c16x, run[q + 1] + run[q + 3]);
-          L = axpy(L, -cx, run[q] + run[q + 4]);
-          L = axpy(L, c16z, qm1[r][q] + qp1[r][q]);
-          L = axpy(L, -cz, qm2[r][q] + zp2[q]);
-          if (DIMS == 3) {
-            L = axpy(L, c16y, ym1[q] + yp1[q]);
-            L = axpy(L, -cy, ym2[q] + yp2[q]);
-          }
+          // sum_d (16 (g-1 + g+1 - 2 g0) - (g-2 + g+2 - 2 g0)) / (12 h_d^2)
+          CT L = lap_wide<DIMS>(c, c16x, cx, c16y, cy, c16z, cz, run[q + 1], run[q + 3], run[q], run[q + 4],
+                               ym1[q], yp1[q], ym2[q], yp2[q], qm1[r][q], qp1[r][q], qm2[r][q], zp2[q]);
           R V;
           if (VARR) V = potential(P, x0 + lx0 + q, y0 + ly0 + r, k);
           else V = (vxr[q] + vyr[r]) + vzk;

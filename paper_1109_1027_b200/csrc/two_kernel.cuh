@@ -123,15 +123,15 @@ __global__ void __launch_bounds__(256) two_step2_kernel(PlaneView<R> T, const cp
       // -1/12 (sum of 2d D-neighbours - (16 - 2d) D) + 1/(6h^2) (edge-midpoints - 4 p Psi)
       L = R(-1.0 / 12.0) * ((sx + sy + sz) - R(16 - 2 * DIMS) * d0);
       if (DIMS >= 2) {
-        cplx<R> e = mk<R>(R(0), R(0));
+        // edge midpoints minus 4 Psi per coordinate plane, the centre subtracted per plane
+        // (each group of four sums to 4 Psi exactly for a constant field, so L = 0 exactly)
         const cplx<R> *zm = T(lz - 1) + o, *zp = T(lz + 1) + o;
+        cplx<R> e = axpy((zm[-1] + zm[1]) + (zp[-1] + zp[1]), R(-4), c);
         if (DIMS == 3) {
-          e = e + (pl[o - P.pitch - 1] + pl[o - P.pitch + 1]) + (pl[o + P.pitch - 1] + pl[o + P.pitch + 1]);
-          e = e + (zm[-P.pitch] + zm[P.pitch]) + (zp[-P.pitch] + zp[P.pitch]);
+          e = e + axpy((pl[o - P.pitch - 1] + pl[o - P.pitch + 1]) + (pl[o + P.pitch - 1] + pl[o + P.pitch + 1]), R(-4), c);
+          e = e + axpy((zm[-P.pitch] + zm[P.pitch]) + (zp[-P.pitch] + zp[P.pitch]), R(-4), c);
         }
-        e = e + (zm[-1] + zm[1]) + (zp[-1] + zp[1]);
-        const int npairs = DIMS * (DIMS - 1) / 2;
-        L = L + Q.w2 * (e - R(4 * npairs) * c);
+        L = L + Q.w2 * e;
       }
     } else {
       L = d0 - R(1.0 / 12.0) * ((sx + sy + sz) - R(2 * DIMS) * d0);

@@ -135,6 +135,45 @@ def test_dirichlet_boundary_values_are_bit_exact():
     assert np.array_equal(out[m], psi[m])
 
 
+@pytest.mark.parametrize("variant", [0, 2, 4, 6])
+@pytest.mark.parametrize("dims,n,dtype,bc,V", [c for c in CASES if c[0] > 1][1::3])
+def test_rk4_parity_isotropic(dims, n, dtype, bc, V, variant):
+    """Equal spacing on every axis selects the kernels' summed-neighbour stencil form."""
+    if variant == 4 and min(n) < 6:
+        pytest.skip("tiny grid")
+    w = _small(dims, n, bc, dtype, V, aniso=False)
+    S = H.gpu_solver(w, dtype, variant)
+    psi = H.psi0_host(w, dtype)
+    P = H.oracle_problem(w)
+    dt = 0.8 * oracle.kmax(P, psi.astype(np.complex128))
+    g = _dev(psi)
+    S.rk4(g, dt, 10)
+    ref = oracle.rk4(P, psi.astype(np.complex128), dt, 10)
+    assert H.rel_l2(g.cpu().numpy(), ref) <= H.TOL[dtype]
+
+
+@pytest.mark.parametrize("dims,n,aniso", [(1, (3000,), True), (2, (300, 70), False), (2, (300, 70), True),
+                                          (3, (80, 40, 20), False), (3, (80, 40, 20), True)])
+@pytest.mark.parametrize("bc", ["dirichlet", "lapzero"])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
+def test_constant_field_is_stationary_to_the_bit(dims, n, aniso, bc, variant):
+    """s = 0, V = 0, Psi = const: the exact Laplacian is 0, so Psi_t = 0 and RK4 must return
+    Psi unchanged.  The stencil is written with the centre inside each difference (lap5 /
+    lap_wide), so with weights rounded to fp32 it still annihilates constants exactly; the
+    separate -30 g0 form left an O(eps) frequency shift per step (C2 c64 drifted 5.8e-5 in 500
+    steps)."""
+    if variant == 4 and dims == 1:
+        pytest.skip("stage pairs: 2D/3D only")
+    w = _small(dims, n, bc, "c64", "none", aniso=aniso)
+    w["s"] = 0.0
+    S = H.gpu_solver(w, "c64", variant)
+    g = torch.full(tuple(reversed(n)), complex(0.6, -0.8), dtype=torch.complex64, device="cuda")
+    g0 = g.clone()
+    S.rk4(g, 0.5 * S.stability_bound(g), 50)
+    assert torch.equal(g, g0)
+    assert torch.count_nonzero(S.laplacian(g0)) == 0
+
+
 # --------------------------------------------------------------------------- configs
 def test_C1_full_2000_steps_and_exact_soliton():
     w = configs.C1()
