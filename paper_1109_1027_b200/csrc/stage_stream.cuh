@@ -78,11 +78,13 @@ template <int SLOT_B, int PT_B> struct Rings {
   static constexpr int RP3 = mn(8, (BUDGET - RT3 * SLOT_B) / (3 * PT_B));
   static_assert(RT0 >= 5 && RP1 >= 2 && RP2 >= 2 && RP3 >= 2, "shared-memory budget too small for the tile");
 };
-// 3D tiles: 28 rows (y-halo overhead 32/28) handled by 14 consumer warps x 2 rows each;
-// chosen by a sweep over (TY, warps, rows/warp) on C4 (scripts/sweep.py).
+// 3D tiles: 24 rows (y-halo overhead 28/24) handled by 12 consumer warps x 2 rows each;
+// chosen by a sweep over (TY, warps, rows/warp) on C4 (scripts/sweep.py; 28 rows / 14 warps
+// until the exact-cancellation stencil R30 made the stage more issue-bound: v18 A/B C4
+// 4.864e10 (28/14) vs 4.895e10 (24/12) vs 4.799e10 (24 rows, 8 warps x 3 rows)).
 #ifndef NLSE3F_TY
-#define NLSE3F_TY 28
-#define NLSE3F_NCW 14
+#define NLSE3F_TY 24
+#define NLSE3F_NCW 12
 #define NLSE3F_RPW 2
 #endif
 template <> struct Cfg<3, float> : Rings<68 * (NLSE3F_TY + 4) * 8, 64 * NLSE3F_TY * 8> {
