@@ -337,9 +337,10 @@ __global__ void NLSE_PAIR_BOUNDS(PLayout<DIMS, R>::NTHREADS)
       }
     }
     // lean planes: no boundary point, no ghost, no array potential in the region a phase covers
-    const bool leanA = P.vkind != 2 && x0 - 2 >= 1 && x0 + TX + 2 <= nx - 1 &&
-                       (DIMS == 2 || (y0 - 2 >= 1 && y0 + TY + 2 <= ny - 1));
-    const bool leanB = P.vkind != 2 && x0 >= 1 && x0 + TX <= nx - 1 && (DIMS == 2 || (y0 >= 1 && y0 + TY <= ny - 1));
+    // (every point in [2, n-3]: the ghosts at -1 and n are read by the points 1 and n-2)
+    const bool leanA = P.vkind != 2 && x0 - 2 >= 2 && x0 + TX + 2 <= nx - 2 &&
+                       (DIMS == 2 || (y0 - 2 >= 2 && y0 + TY + 2 <= ny - 2));
+    const bool leanB = P.vkind != 2 && x0 >= 2 && x0 + TX <= nx - 2 && (DIMS == 2 || (y0 >= 2 && y0 + TY <= ny - 2));
 
     CT qm2[RPW][PPX], qm1[RPW][PPX], qp1[RPW][PPX];
     cplx<R> *outT = P.out_T + int64_t(kb) * P.plane + int64_t(y0 + ly0) * P.pitch + (x0 + lx0);

@@ -505,7 +505,9 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
     // tile facts (CTA-uniform)
     const bool xlo = x0 == 0, xhi = (x0 <= nx - 2) && (nx - 2 < x0 + TX);
     const bool ylo = DIMS == 3 && y0 == 0, yhi = DIMS == 3 && (y0 <= ny - 2) && (ny - 2 < y0 + TY);
-    const bool inner_xy = x0 >= 1 && x0 + TX <= nx - 1 && (DIMS == 2 || (y0 >= 1 && y0 + TY <= ny - 1));
+    // every point of the tile in [2, n-3] on x (and y): none is a boundary point and none reads a
+    // ghost (the ghosts at -1 and n are read by the points 1 and n-2)
+    const bool inner_xy = x0 >= 2 && x0 + TX <= nx - 2 && (DIMS == 2 || (y0 >= 2 && y0 + TY <= ny - 2));
 
     // per-thread potential tables of this tile (harmonic V is separable)
     R vxr[PPX], vyr[RPW];

@@ -174,6 +174,30 @@ def test_constant_field_is_stationary_to_the_bit(dims, n, aniso, bc, variant):
     assert torch.count_nonzero(S.laplacian(g0)) == 0
 
 
+@pytest.mark.parametrize("variant", [0, 2, 4])
+@pytest.mark.parametrize("dims,n,dtype", [
+    (3, (129, 49, 9), "c64"),    # x0 + TX = nx - 1 and y0 + TY = ny - 1 (64 x 24 tiles)
+    (3, (97, 65, 9), "c128"),    # the same for 32 x 32 tiles
+    (3, (130, 50, 9), "c64"), (3, (128, 48, 9), "c64"),
+    (2, (2049, 9), "c64"), (2, (1025, 9), "c128"),  # 1024 / 512-wide 2D rows
+])
+def test_tile_edge_one_short_of_the_face(dims, n, dtype, variant):
+    """A tile whose last column (row) is nx-2 (ny-2) reads the ghost at nx (ny): such tiles must
+    not take the interior ("lean") path that reads the halo straight from the grid."""
+    w = _small(dims, n, "dirichlet", dtype, "harmonic")
+    S = H.gpu_solver(w, dtype, variant)
+    psi = H.psi0_host(w, dtype)
+    P = H.oracle_problem(w)
+    dt = 0.8 * oracle.kmax(P, psi.astype(np.complex128))
+    g = _dev(psi)
+    S.rk4(g, dt, 3)
+    ref = oracle.rk4(P, psi.astype(np.complex128), dt, 3)
+    assert H.rel_l2(g.cpu().numpy(), ref) <= H.TOL[dtype]
+    L = S.laplacian(_dev(psi)).cpu().numpy()
+    Lo = oracle.laplacian(P, psi.astype(np.complex128))
+    assert H.rel_l2(L, Lo) <= (1e-12 if dtype == "c128" else 1e-5)
+
+
 # --------------------------------------------------------------------------- configs
 def test_C1_full_2000_steps_and_exact_soliton():
     w = configs.C1()
