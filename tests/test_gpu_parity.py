@@ -198,6 +198,28 @@ def test_tile_edge_one_short_of_the_face(dims, n, dtype, variant):
     assert H.rel_l2(L, Lo) <= (1e-12 if dtype == "c128" else 1e-5)
 
 
+@pytest.mark.parametrize("dims,dtype,TX,TY", [(3, "c64", 64, 24), (3, "c128", 32, 32), (2, "c64", 1024, 1),
+                                           (2, "c128", 512, 1)])
+def test_tile_edge_sweep(dims, dtype, TX, TY):
+    """Every grid size within +-2 of a two-tile multiple on x (and y in 3D), both BCs, fused and
+    stage-pair kernels, against the oracle: all tile/face/ghost combinations at the far edge."""
+    nxs = [2 * TX + d for d in range(-2, 3)]
+    nys = [2 * TY + d for d in range(-2, 3)] if dims == 3 else [9]
+    for i, (nx, ny) in enumerate([(a, b) for a in nxs for b in nys]):
+        n = (nx, ny, 7) if dims == 3 else (nx, ny)
+        bc = ("dirichlet", "lapzero")[i % 2]
+        w = _small(dims, n, bc, dtype, "harmonic")
+        psi = H.psi0_host(w, dtype)
+        P = H.oracle_problem(w)
+        dt = 0.8 * oracle.kmax(P, psi.astype(np.complex128))
+        ref = oracle.rk4(P, psi.astype(np.complex128), dt, 2)
+        for v in (0, 4):
+            S = H.gpu_solver(w, dtype, v)
+            g = _dev(psi)
+            S.rk4(g, dt, 2)
+            assert H.rel_l2(g.cpu().numpy(), ref) <= H.TOL[dtype], (n, bc, v)
+
+
 # --------------------------------------------------------------------------- configs
 def test_C1_full_2000_steps_and_exact_soliton():
     w = configs.C1()
