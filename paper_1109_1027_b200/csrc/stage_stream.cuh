@@ -764,8 +764,9 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
     // faces (no boundary point, no ghost): straight-line loads, arithmetic and stores.
     const CT *ringT = ring + toff;
     const int64_t pitch = P.pitch, plane = P.plane;
-    auto lean_step = [&](int k, auto varr_c) {
+    auto lean_step = [&](int k, auto varr_c, auto xf_c) {
       constexpr bool VARR = decltype(varr_c)::value;  // array potential (else separable tables)
+      constexpr bool XF = decltype(xf_c)::value;      // x-face tile: ghost fill + boundary column
       const int gz = z0 + k;
       const R vzk = vz_next(k);
       mbar_wait(&fullT[sk2], ph2);
@@ -773,6 +774,27 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
       if (NPA) {
         mbar_wait(&fullP[sp], php);
         pa = pring + size_t(sp) * NPA * LY::PTILE + ly0 * TX + lx0;
+      }
+      if (XF) {
+        // x-face ghosts of this plane, exactly as the general step forms them (reading R8)
+        CT *g0 = tslot(k), *gm = tslot(k - 1), *gp = tslot(k + 1);
+        auto at = [&](CT *s_, int lx, int ly) -> CT & { return s_[(ly + HY) * W + lx + 2]; };
+        auto owner = [&](int lx, int ly) { return ((ly / RPW) * CPT + lx / PPX) >> 5; };
+#pragma unroll
+        for (int hi = 0; hi < 2; ++hi) {
+          if (hi ? !xhi : !xlo) continue;
+          const int bx = hi ? nx - 1 : 0, lb = bx - x0, n = hi ? -1 : 1;
+          for (int ly = lane; ly < TY; ly += 32) {
+            if (owner(lb + n, ly) != warp) continue;
+            CT cbv = at(g0, lb, ly), cin = at(g0, lb + n, ly);
+            CT D = lambda_b(P, cbv, potential(P, bx, y0 + ly, k));
+            D = D - d2(at(gm, lb, ly), cbv, at(gp, lb, ly), P.ihz2);
+            if (DIMS == 3) D = D - d2(at(g0, lb, ly - 1), cbv, at(g0, lb, ly + 1), P.ihy2);
+            at(g0, lb - n, ly) = axpy(R(2) * cbv - cin, P.hx2, D);
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
       }
       const CT *s0 = ringT + size_t(sk) * LY::SLOT, *sp2 = ringT + size_t(sk2) * LY::SLOT;
       CT ym2[PPX], ym1[PPX], yp1[PPX], yp2[PPX], cprev[PPX];  // y window, rolled down the rows
@@ -815,7 +837,11 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
           if (VARR) V = potential(P, x0 + lx0 + q, y0 + ly0 + r, k);
           else V = (vxr[q] + vyr[r]) + vzk;
           const R N = fma(ps_, norm2(c), -V);
-          const CT tF = axpy(N * c, pa_, L);  // F = i (a L + N c)
+          CT tF = axpy(N * c, pa_, L);  // F = i (a L + N c)
+          if (XF && (x0 + lx0 + q == 0 || x0 + lx0 + q == nx - 1)) {  // boundary column (face rule)
+            L = lambda_b(P, c, V);
+            tF = P.bc == 0 ? zero : N * c;
+          }
           if (MODE == M_LAP) {
             oT[q] = L;
           } else if (MODE == M_S1) {
@@ -875,6 +901,13 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
 #else
 #define NLSE_LEAN_OK false
 #endif
+#ifndef NLSE_XFACE_LEAN
+#define NLSE_XFACE_LEAN 1
+#endif
+    // x-face tiles (3D, full in x, interior in y, separable V): the lean step plus the x-face
+    // ghost fill and the boundary column's face rule; bit-identical to the general step
+    const bool xface_lean = NLSE_XFACE_LEAN && NLSE_LEAN_OK && DIMS == 3 && !inner_xy && (xlo || xhi) &&
+                            P.vkind != 2 && x0 + TX <= nx && y0 >= 2 && y0 + TY <= ny - 2;
     if (inner_xy && NLSE_LEAN_OK && (NLSE_LEAN_DIMS & DIMS)) {
       // lean planes: gz in [2, NZ-3], clamped to this tile's chunk [kb, ke)
       const int l0 = min(ke, max(kb, 2 - z0)), l1 = max(l0, min(ke, NZ - 2 - z0));
@@ -886,12 +919,20 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
       constexpr int kLU = NLSE_LEAN_UNROLL;
       if (P.vkind == 2) {
 #pragma unroll (kLU)
-        for (; k < l1; ++k) lean_step(k, std::true_type{});
+        for (; k < l1; ++k) lean_step(k, std::true_type{}, std::false_type{});
       } else {
 #pragma unroll (kLU)
-        for (; k < l1; ++k) lean_step(k, std::false_type{});
+        for (; k < l1; ++k) lean_step(k, std::false_type{}, std::false_type{});
       }
       for (; k < ke; ++k) general_step(k);
+    } else if (DIMS == 3 && xface_lean) {
+      if constexpr (DIMS == 3) {
+        const int l0 = min(ke, max(kb, 2 - z0)), l1 = max(l0, min(ke, NZ - 2 - z0));
+        int k = kb;
+        for (; k < l0; ++k) general_step(k);
+        for (; k < l1; ++k) lean_step(k, std::false_type{}, std::true_type{});
+        for (; k < ke; ++k) general_step(k);
+      }
     } else {
       for (int k = kb; k < ke; ++k) general_step(k);
     }
