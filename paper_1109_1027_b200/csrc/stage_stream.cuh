@@ -766,7 +766,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
     const int64_t pitch = P.pitch, plane = P.plane;
     auto lean_step = [&](int k, auto varr_c, auto xf_c) {
       constexpr bool VARR = decltype(varr_c)::value;  // array potential (else separable tables)
-      constexpr bool XF = decltype(xf_c)::value;      // x-face tile: ghost fill + boundary column
+      constexpr bool XF = decltype(xf_c)::value;      // face tile: ghost fill + boundary rows/columns
       const int gz = z0 + k;
       const R vzk = vz_next(k);
       mbar_wait(&fullT[sk2], ph2);
@@ -776,7 +776,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
         pa = pring + size_t(sp) * NPA * LY::PTILE + ly0 * TX + lx0;
       }
       if (XF) {
-        // x-face ghosts of this plane, exactly as the general step forms them (reading R8)
+        // face ghosts of this plane, exactly as the general step forms them (reading R8)
         CT *g0 = tslot(k), *gm = tslot(k - 1), *gp = tslot(k + 1);
         auto at = [&](CT *s_, int lx, int ly) -> CT & { return s_[(ly + HY) * W + lx + 2]; };
         auto owner = [&](int lx, int ly) { return ((ly / RPW) * CPT + lx / PPX) >> 5; };
@@ -785,12 +785,29 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
           if (hi ? !xhi : !xlo) continue;
           const int bx = hi ? nx - 1 : 0, lb = bx - x0, n = hi ? -1 : 1;
           for (int ly = lane; ly < TY; ly += 32) {
-            if (owner(lb + n, ly) != warp) continue;
+            const int gy = y0 + ly;
+            if (gy < 1 || gy > ny - 2 || owner(lb + n, ly) != warp) continue;
             CT cbv = at(g0, lb, ly), cin = at(g0, lb + n, ly);
-            CT D = lambda_b(P, cbv, potential(P, bx, y0 + ly, k));
+            CT D = lambda_b(P, cbv, potential(P, bx, gy, k));
             D = D - d2(at(gm, lb, ly), cbv, at(gp, lb, ly), P.ihz2);
             if (DIMS == 3) D = D - d2(at(g0, lb, ly - 1), cbv, at(g0, lb, ly + 1), P.ihy2);
             at(g0, lb - n, ly) = axpy(R(2) * cbv - cin, P.hx2, D);
+          }
+        }
+        if (DIMS == 3) {
+#pragma unroll
+          for (int hi = 0; hi < 2; ++hi) {
+            if (hi ? !yhi : !ylo) continue;
+            const int by = hi ? ny - 1 : 0, lb = by - y0, n = hi ? -1 : 1;
+            for (int lx = lane; lx < TX; lx += 32) {
+              const int gx = x0 + lx;
+              if (gx < 1 || gx > nx - 2 || owner(lx, lb + n) != warp) continue;
+              CT cbv = at(g0, lx, lb), cin = at(g0, lx, lb + n);
+              CT D = lambda_b(P, cbv, potential(P, gx, by, k));
+              D = D - d2(at(gm, lx, lb), cbv, at(gp, lx, lb), P.ihz2);
+              D = D - d2(at(g0, lx - 1, lb), cbv, at(g0, lx + 1, lb), P.ihx2);
+              at(g0, lx, lb - n) = axpy(R(2) * cbv - cin, P.hy2, D);
+            }
           }
         }
         fence_proxy_async_smem();
@@ -838,7 +855,8 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
           else V = (vxr[q] + vyr[r]) + vzk;
           const R N = fma(ps_, norm2(c), -V);
           CT tF = axpy(N * c, pa_, L);  // F = i (a L + N c)
-          if (XF && (x0 + lx0 + q == 0 || x0 + lx0 + q == nx - 1)) {  // boundary column (face rule)
+          if (XF && (x0 + lx0 + q == 0 || x0 + lx0 + q == nx - 1 || y0 + ly0 + r == 0 ||
+                     y0 + ly0 + r == ny - 1)) {  // boundary column / row (face rule)
             L = lambda_b(P, c, V);
             tF = P.bc == 0 ? zero : N * c;
           }
@@ -904,10 +922,10 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
 #ifndef NLSE_XFACE_LEAN
 #define NLSE_XFACE_LEAN 1
 #endif
-    // x-face tiles (3D, full in x, interior in y, separable V): the lean step plus the x-face
-    // ghost fill and the boundary column's face rule; bit-identical to the general step
-    const bool xface_lean = NLSE_XFACE_LEAN && NLSE_LEAN_OK && DIMS == 3 && !inner_xy && (xlo || xhi) &&
-                            P.vkind != 2 && x0 + TX <= nx && y0 >= 2 && y0 + TY <= ny - 2;
+    // face tiles (3D, full in x and y, separable V): the lean step plus the x/y-face ghost fill
+    // and the face rule on the boundary columns/rows; bit-identical to the general step
+    const bool xface_lean = NLSE_XFACE_LEAN && NLSE_LEAN_OK && DIMS == 3 && !inner_xy && P.vkind != 2 &&
+                            x0 + TX <= nx && y0 + TY <= ny;
     if (inner_xy && NLSE_LEAN_OK && (NLSE_LEAN_DIMS & DIMS)) {
       // lean planes: gz in [2, NZ-3], clamped to this tile's chunk [kb, ke)
       const int l0 = min(ke, max(kb, 2 - z0)), l1 = max(l0, min(ke, NZ - 2 - z0));
