@@ -160,6 +160,34 @@ nlse2shoc_status nlse2shoc_set_variant(nlse2shoc_t, int variant);
 typedef enum { NLSE2SHOC_SCHEME_2SHOC = 0, NLSE2SHOC_SCHEME_CD = 1 } nlse2shoc_scheme;
 nlse2shoc_status nlse2shoc_set_scheme(nlse2shoc_t, int scheme);
 
+/* Execution-path options of a handle (applied to every later call; a loopback handle passes
+ * them to its virtual slabs).  None changes the arithmetic of a point: every option selects
+ * between code paths that evaluate the same expressions, so results are bit-identical
+ * unless noted.  Defaults in brackets.
+ *  CUDA_GRAPH    [1] single-slab rk4 calls of >= 4 steps capture one step's launches in a
+ *                    CUDA graph and replay it (fewer launch overheads).
+ *  OVERLAP       [1] sharded / loopback 2D-3D fused variants: edge planes first, halo
+ *                    exchange on a side stream beside the interior planes.
+ *  RESIDENT_1D   [1] small 1D grids (4 fields <= 200 KB) run the whole call in one CTA.
+ *  REVERSE_ORDER [1] stages 2 and 4 walk the tiles backwards (L2 reuse).  Changes the
+ *                    order of nothing but the tiles: bit-identical.
+ *  LEAN_STEPS    [3] branch-free plane steps of the fused 2D/3D kernel: bit 1 = tiles with
+ *                    no boundary point and no ghost, bit 2 = 3D tiles touching an x/y face
+ *                    (ghost fill + face rule inline).  0 = the general step everywhere.
+ *  ZCHUNKS       [0] fused 2D/3D kernels: number of chunks the streamed axis is split into
+ *                    (0 = automatic); values that would leave empty chunks are reduced to the
+ *                    smallest count with the same chunk length.
+ * EINVAL for an unknown option or a negative value.                                     */
+typedef enum {
+  NLSE2SHOC_OPT_CUDA_GRAPH = 0,
+  NLSE2SHOC_OPT_OVERLAP = 1,
+  NLSE2SHOC_OPT_RESIDENT_1D = 2,
+  NLSE2SHOC_OPT_REVERSE_ORDER = 3,
+  NLSE2SHOC_OPT_LEAN_STEPS = 4,
+  NLSE2SHOC_OPT_ZCHUNKS = 5
+} nlse2shoc_option;
+nlse2shoc_status nlse2shoc_set_option(nlse2shoc_t, int option, int64_t value);
+
 /* L = Lap(psi) by 2SHOC; boundary points get L_b = lambda_b.  psi, L: device,
  * field layout, distinct.  Sharded: halo exchange included (collective).             */
 nlse2shoc_status nlse2shoc_laplacian(nlse2shoc_t, const void *psi, void *L, void *stream);

@@ -14,7 +14,7 @@ from ._lib import BC, DTYPE, VKIND, NLSE2SHOCError, Potential, check, lib
 __all__ = [
     "Solver", "NLSE2SHOCError", "nlse2shoc_create", "nlse2shoc_create_sharded", "nlse2shoc_get_unique_id",
     "nlse2shoc_laplacian", "nlse2shoc_rk4", "nlse2shoc_stability_bound", "nlse2shoc_check_finite",
-    "nlse2shoc_split", "nlse2shoc_version", "solver_from_work", "nlse2shoc_create_loopback",
+    "nlse2shoc_split", "nlse2shoc_version", "solver_from_work", "nlse2shoc_create_loopback", "nlse2shoc_set_option",
 ]
 
 
@@ -119,6 +119,40 @@ def nlse2shoc_check_finite(H, psi, stream=None):
     check(lib().nlse2shoc_check_finite(H, _ptr(psi), _stream(stream)), "check_finite")
 
 
+OPTIONS = {"cuda_graph": 0, "overlap": 1, "resident_1d": 2, "reverse_order": 3, "lean_steps": 4, "zchunks": 5}
+
+
+def nlse2shoc_set_option(H, option, value: int):
+    check(lib().nlse2shoc_set_option(H, OPTIONS.get(option, option), int(value)), "set_option")
+
+
+def _check_V_array(V, dims, N, dtype, shard):
+    """V kind 'array' reaches the library as a raw pointer that the kernels read as R (float32
+    for c64, float64 for c128) over the whole grid (single-GPU / loopback handles) or the
+    local z-slab (NCCL shards): check what the pointer cannot carry."""
+    import torch
+
+    t = V.get("data") if V else None
+    if t is None or not isinstance(t, torch.Tensor):
+        raise ValueError("V['data'] must be a torch tensor for V kind 'array'")
+    want = torch.float32 if dtype == "c64" else torch.float64
+    if not t.is_cuda or t.device.index != torch.cuda.current_device():
+        raise ValueError(f"V['data'] must be a CUDA tensor on device {torch.cuda.current_device()}")
+    if t.dtype != want:
+        raise ValueError(f"V['data'] has dtype {t.dtype}, the handle computes in {want}")
+    if not t.is_contiguous():
+        raise ValueError("V['data'] must be contiguous ([z][y][x], x fastest)")
+    n = [int(v) for v in list(N)[:dims]]
+    total = 1
+    for v in n:
+        total *= v
+    if shard is not None and "loopback" not in shard:
+        _, nz = nlse2shoc_split(n[-1], shard["nranks"], shard["rank"])
+        total = total // n[-1] * nz
+    if t.numel() != total:
+        raise ValueError(f"V['data'] has {t.numel()} values, expected {total}")
+
+
 class Solver:
     """Owns one nlse2shoc handle.  Psi tensors are contiguous torch complex64/complex128
     CUDA tensors of shape (Nz, Ny, Nx) / (Ny, Nx) / (Nx,) (sharded: the local slab)."""
@@ -126,6 +160,8 @@ class Solver:
     def __init__(self, dims, N, h, a, s, V=None, bc="dirichlet", dtype="c64", shard=None):
         self.dims, self.dtype, self.bc = int(dims), dtype, bc
         self.N = [int(v) for v in list(N)[:dims]]
+        if V is not None and V.get("kind") == "array":
+            _check_V_array(V, self.dims, N, dtype, shard)
         if shard is None:
             self._h, self._keep = nlse2shoc_create(dims, N, h, a, s, V, bc, dtype)
         elif "loopback" in shard:
@@ -147,6 +183,11 @@ class Solver:
 
     def set_variant(self, variant: int):
         check(lib().nlse2shoc_set_variant(self._h, int(variant)), "set_variant")
+
+    def set_option(self, option, value: int):
+        """Execution-path option (include/nlse2shoc.h nlse2shoc_option): 'cuda_graph',
+        'overlap', 'resident_1d', 'reverse_order', 'lean_steps', 'zchunks'."""
+        nlse2shoc_set_option(self._h, option, value)
 
     def set_scheme(self, scheme):
         """0/"2shoc" (default) or 1/"cd" (the paper's RK4+CD comparison scheme)."""

@@ -118,23 +118,9 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t *bar, uint32_t parity
   }
 }
 
-// 2D / 3D tiled TMA load global -> shared, completion counted on an mbarrier.
-__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-      : "memory");
-}
-// Same loads with an L2 eviction-priority policy (createpolicy), e.g. evict_first for
-// read-once streams so that the stencil input planes stay resident for neighbour halos.
+// 2D / 3D tiled TMA loads global -> shared with an L2 eviction-priority policy (createpolicy),
+// completion counted on an mbarrier; e.g. evict_first for read-once streams so that the
+// stencil input planes stay resident for neighbour halos.
 __device__ __forceinline__ void tma_load_2d_hint(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
                                                  uint64_t pol) {
   asm volatile(
@@ -181,55 +167,13 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
-// streaming (evict-first) 128-bit global stores: outputs are re-read only by the next stage
-#ifndef NLSE_STORE_KIND
-#define NLSE_STORE_KIND 0
-#endif
-#if NLSE_STORE_KIND == 1
-__device__ __forceinline__ void st_stream(float4 *p, float4 v) { __stcs(p, v); }
-__device__ __forceinline__ void st_stream(double2 *p, double2 v) { __stcs(p, v); }
-#elif NLSE_STORE_KIND == 2
-__device__ __forceinline__ void st_stream(float4 *p, float4 v) { __stwt(p, v); }
-__device__ __forceinline__ void st_stream(double2 *p, double2 v) { __stwt(p, v); }
-#else
+// 128-bit global stores of the stage outputs (plain stores: evict-first / write-through
+// variants measured no faster on C4 / C5W, profiles/r01/README.md)
 __device__ __forceinline__ void st_stream(float4 *p, float4 v) { *p = v; }
 __device__ __forceinline__ void st_stream(double2 *p, double2 v) { *p = v; }
-#endif
-
-// accumulator stores (NLSE_ACC_STORE=1: evict-first, since acc is re-read only two stages
-// later; measured no better than plain stores on C4 / C5W, so plain is the default)
-#ifndef NLSE_ACC_STORE
-#define NLSE_ACC_STORE 0
-#endif
-#if NLSE_ACC_STORE == 1
-__device__ __forceinline__ void st_acc(float4 *p, float4 v) { __stcs(p, v); }
-__device__ __forceinline__ void st_acc(double2 *p, double2 v) { __stcs(p, v); }
-#else
-__device__ __forceinline__ void st_acc(float4 *p, float4 v) { *p = v; }
-__device__ __forceinline__ void st_acc(double2 *p, double2 v) { *p = v; }
-#endif
-
-__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t *p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed_gpu(uint32_t *p, uint32_t v) {
-  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
-__device__ __forceinline__ bool elect_one() {
-  uint32_t pred = 0;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "elect.sync _|p, 0xffffffff;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(pred));
-  return pred != 0;
 }
 
 }  // namespace nlse

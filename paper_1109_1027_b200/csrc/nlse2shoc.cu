@@ -108,6 +108,9 @@ struct nlse2shoc_s {
   size_t bytes = 0;
   int num_sms = 148;
   int64_t launches = 0;
+  // execution-path options (nlse2shoc_set_option): results are the same up to the rounding
+  // differences stated in include/nlse2shoc.h
+  int opt_graph = 1, opt_overlap = 1, opt_resident = 1, opt_reverse = 1, opt_lean = 3, opt_zchunks = 0;
   // loopback (single-GPU emulation of z-slab sharding, SURVEY §4 T3'): virtual slabs that
   // exchange halos by device copies instead of NCCL; empty for ordinary handles
   std::vector<nlse2shoc_s *> slabs;
@@ -169,27 +172,12 @@ static nlse2shoc_status encode_map(CUtensorMap *tm, void *base, int dims_tensor,
   return NLSE2SHOC_OK;
 }
 
-// L2 promotion of the stencil-input (halo) boxes; NLSE_TMA_PROMO=0/64/128/256 overrides.
-// Default 64 B: a halo column's 16-byte row piece then brings in its whole 64-byte DRAM
-// burst, which the x-neighbour tile's halo read hits in L2 (C4: 9.75 -> 9.48 ms/step;
-// none and 256 B measured worse).
-static CUtensorMapL2promotion promo_of(int v) {
-  return v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-                 : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
-                            : v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_NONE;
-}
-// pointwise (Psi^n / acc) boxes; NLSE_TMA_PROMO_P overrides (default 256 B)
-static CUtensorMapL2promotion tma_promo_p() {
-  const char *e = getenv("NLSE_TMA_PROMO_P");
-  return promo_of(e ? atoi(e) : 256);
-}
-static CUtensorMapL2promotion tma_promo() {
-  const char *e = getenv("NLSE_TMA_PROMO");
-  int v = e ? atoi(e) : 64;
-  return v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-                 : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
-                            : v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_NONE;
-}
+// L2 promotion of the stencil-input (halo) boxes: 64 B, so a halo column's 16-byte row piece
+// brings in its whole 64-byte DRAM burst, which the x-neighbour tile's halo read hits in L2
+// (C4: 9.75 -> 9.48 ms/step; none and 256 B measured worse).  Pointwise (Psi^n / acc) boxes:
+// 256 B.
+static CUtensorMapL2promotion tma_promo() { return CU_TENSOR_MAP_L2_PROMOTION_L2_64B; }
+static CUtensorMapL2promotion tma_promo_p() { return CU_TENSOR_MAP_L2_PROMOTION_L2_256B; }
 
 template <int DIMS, typename R> struct Maps {
   using LY = Layout<DIMS, R>;
@@ -277,6 +265,7 @@ template <typename R> static void fill_params(nlse2shoc_t H, StageParams<R> &P) 
   P.s = R(H->s);
   P.inv_a = R(1.0 / H->a);
   P.bc = H->bc;
+  P.lean = H->opt_lean;
   P.vkind = int(H->V.kind);
   if (H->V.kind == NLSE2SHOC_V_HARMONIC) {
     const R *t = reinterpret_cast<const R *>(H->vtab);
@@ -312,6 +301,15 @@ template <int DIMS, typename R, int MODE> static nlse2shoc_status set_smem_attr(
   return NLSE2SHOC_OK;
 }
 
+// The kernels give chunk c the planes [c L, min((c+1) L, n)) with L = ceil(n / nchunk): a count
+// whose last chunks would start at or past n (e.g. n = 33, nchunk = 8: L = 5, chunk 7 starts
+// at 35) is replaced by the smallest count with the same L, so every chunk is non-empty.
+static int zchunks_normalised(int n, int nchunk) {
+  if (n <= 0 || nchunk <= 1) return 1;
+  const int L = (n + nchunk - 1) / nchunk;
+  return (n + L - 1) / L;
+}
+
 template <int DIMS, typename R, int MODE>
 static nlse2shoc_status launch_stream(nlse2shoc_t H, Field &in, const CUtensorMap *tm_psi, const CUtensorMap *tm_acc,
                                       StageParams<R> P, cudaStream_t st, const CUtensorMap *tm_t3 = nullptr) {
@@ -340,8 +338,8 @@ static nlse2shoc_status launch_stream(nlse2shoc_t H, Field &in, const CUtensorMa
     if ((DIMS != 3 || len - 1.5 <= 64.0) && c < bestc - 1e-9) { bestc = c; best = nc; }
   }
   if (bestc > 1e299) best = best_any;
-  static const int force_chunks = getenv("NLSE_NCHUNK") ? atoi(getenv("NLSE_NCHUNK")) : 0;
-  if (force_chunks > 0) best = std::min<int>(force_chunks, nzr);
+  if (H->opt_zchunks > 0) best = std::min<int>(H->opt_zchunks, nzr);
+  best = std::max(1, zchunks_normalised(nzr, best));
   P.nchunk = best;
   P.ntiles = ncol * best;
   const int G = std::min(G0, P.ntiles);
@@ -383,8 +381,8 @@ static nlse2shoc_status launch_pair(nlse2shoc_t H, const CUtensorMap &tin, const
     const double c = rounds * (std::ceil(double(H->nz) / nc) + 4.0);
     if (c < bestc - 1e-9) { bestc = c; best = nc; }
   }
-  static const int force_chunks = getenv("NLSE_NCHUNK") ? atoi(getenv("NLSE_NCHUNK")) : 0;
-  if (force_chunks > 0) best = std::min<int>(force_chunks, int(H->nz));
+  if (H->opt_zchunks > 0) best = std::min<int>(H->opt_zchunks, int(H->nz));
+  best = zchunks_normalised(int(H->nz), best);
   P.nchunk = best;
   P.ntiles = ncol * best;
   const int G = std::min(G0, P.ntiles);
@@ -430,24 +428,12 @@ template <typename R, int MODE>
 static nlse2shoc_status launch_line(nlse2shoc_t H, const void *in, const void *psi, const void *acc, StageParams<R> P,
                                     cudaStream_t st, const void *t3 = nullptr) {
   const int threads = 256;
-  // complex128: the grid-stride kernel (L1 serves the stencil overlap) measured faster than the
-  // shared-memory tiles on C2 (0.191 vs 0.205-0.230 ms/step); complex64: tiles of 256 points
-  // (C2 0.110 ms; 512 / 1024 / 2048-point tiles 0.128 / 0.119 / 0.115, grid-stride 0.125)
-#ifndef NLSE_LINE_TILE_C128
-#define NLSE_LINE_TILE_C128 0
-#endif
-#ifndef NLSE_LINE_PT
-#define NLSE_LINE_PT 1
-#endif
-#ifndef NLSE_LINE_STREAM
-#define NLSE_LINE_STREAM 1
-#endif
   // complex128 grids of >= 16 segments: the persistent bulk-copy ring (C2 0.187 -> 0.152 ms per
-  // step); complex64 keeps the 256-point tiles (0.109 vs 0.113 ms with the ring)
-#ifndef NLSE_LINE_STREAM64
-#define NLSE_LINE_STREAM64 0
-#endif
-  if (NLSE_LINE_STREAM && (sizeof(R) == 8 || NLSE_LINE_STREAM64) && H->nx >= 16 * LineStream<R>::SEG) {
+  // step); smaller complex128 grids: the grid-stride kernel (L1 serves the stencil overlap;
+  // faster than shared-memory tiles, C2 0.191 vs 0.205-0.230 ms/step); complex64: tiles of 256
+  // points (C2 0.110 ms; 512 / 1024 / 2048-point tiles 0.128 / 0.119 / 0.115, grid-stride
+  // 0.125, the ring 0.113)
+  if (sizeof(R) == 8 && H->nx >= 16 * LineStream<R>::SEG) {
     static std::atomic<uint64_t> attr{0};
     const size_t smem = line_stream_smem<R, MODE>();
     if (attr_needed(attr)) {
@@ -459,13 +445,13 @@ static nlse2shoc_status launch_line(nlse2shoc_t H, const void *in, const void *p
     line_stream_kernel<R, MODE><<<grid, LineStream<R>::NT, smem, st>>>(
         reinterpret_cast<const cplx<R> *>(in), reinterpret_cast<const cplx<R> *>(psi),
         reinterpret_cast<const cplx<R> *>(acc), reinterpret_cast<const cplx<R> *>(t3), P);
-  } else if (sizeof(R) == 8 && !NLSE_LINE_TILE_C128) {
+  } else if (sizeof(R) == 8) {
     const int64_t blocks = std::min<int64_t>((H->nx + threads - 1) / threads, int64_t(H->num_sms) * 8);
     stage_line_kernel<R, MODE><<<int(blocks), threads, 0, st>>>(
         reinterpret_cast<const cplx<R> *>(in), reinterpret_cast<const cplx<R> *>(psi),
         reinterpret_cast<const cplx<R> *>(acc), reinterpret_cast<const cplx<R> *>(t3), P);
   } else {
-    constexpr int PT = NLSE_LINE_PT;
+    constexpr int PT = 1;
     const int64_t blocks = (H->nx + threads * PT - 1) / (threads * PT);
     line_tile_kernel<R, MODE, PT><<<int(blocks), threads, 0, st>>>(
         reinterpret_cast<const cplx<R> *>(in), reinterpret_cast<const cplx<R> *>(psi),
@@ -556,9 +542,8 @@ static nlse2shoc_status launch_stage(nlse2shoc_t H, Field &psi, int s, double dt
   StageParams<R> P;
   fill_params<R>(H, P);
   // stages 2 and 4 walk the grid backwards: the planes the previous stage wrote last are still
-  // in L2 when this stage starts (NLSE_NO_REV=1 disables)
-  static const bool no_rev = getenv("NLSE_NO_REV") != nullptr;
-  P.rev = (!no_rev && (s == 2 || s == 4)) ? 1 : 0;
+  // in L2 when this stage starts (option REVERSE_ORDER)
+  P.rev = (H->opt_reverse && (s == 2 || s == 4)) ? 1 : 0;
   // base pointers of the pointwise streams (must match the maps passed to launch_stream)
   P.in_P[0] = reinterpret_cast<const cplx<R> *>(psi.ptr);
   P.in_P[1] = reinterpret_cast<const cplx<R> *>(H->acc.ptr);
@@ -692,19 +677,17 @@ template <typename R> static nlse2shoc_status rk4_resident_1d(nlse2shoc_t H, Fie
 
 static bool resident_ok(nlse2shoc_t H) {
   return H->dims == 1 && H->slabs.empty() && !H->sharded && H->variant != 1 && H->variant != 3 &&
-         size_t(4) * size_t(H->nx) * H->S <= size_t(200) * 1024 && !getenv("NLSE_NO_RESIDENT");
+         size_t(4) * size_t(H->nx) * H->S <= size_t(200) * 1024 && H->opt_resident;
 }
 
 // Edge-first halo exchange: per stage, the 2 edge planes at each slab end
 // (the ones that read halos and that the neighbours need) are computed first, their exchange
 // runs on a side stream while the interior planes are computed, and the next stage's edges
-// wait for it.  Fused 2D/3D variants (0, 2) on slabs of >= 8 planes; NLSE_NO_OVERLAP=1 off.
+// wait for it.  Fused 2D/3D variants on slabs of >= 8 planes (option OVERLAP).
 static bool overlap_ok(const View &v) {
-  static const bool off = getenv("NLSE_NO_OVERLAP") != nullptr;
-  if (off) return false;
   bool multi = v.hs.size() > 1;
   for (nlse2shoc_t H : v.hs) {
-    if (H->dims < 2 || (H->variant != 0 && H->variant != 2 && H->variant != 5 && H->variant != 6) || H->nz < 8)
+    if (!H->opt_overlap || H->dims < 2 || (H->variant != 0 && H->variant != 2 && H->variant != 5 && H->variant != 6) || H->nz < 8)
       return false;
     multi = multi || (H->sharded && H->nranks > 1);
   }
@@ -755,11 +738,7 @@ static nlse2shoc_status run_rk4_overlapped(View &v, double dt, int64_t nsteps, c
 
 // Single-slab calls of >= 4 steps: the four stage launches of one step are captured once
 // into a CUDA graph (on a private stream) and the graph is replayed nsteps times on the
-// caller's stream, which trims per-launch overhead on small grids (NLSE_NO_GRAPH=1: off).
-static bool graph_ok() {
-  static const bool off = getenv("NLSE_NO_GRAPH") != nullptr;
-  return !off;
-}
+// caller's stream, which trims per-launch overhead on small grids (option CUDA_GRAPH).
 
 static nlse2shoc_status run_rk4_graph(View &v, double dt, int64_t nsteps, cudaStream_t st) {
   nlse2shoc_t H = v.hs[0];
@@ -795,7 +774,7 @@ static nlse2shoc_status run_rk4(View &v, double dt, int64_t nsteps, cudaStream_t
                                      : rk4_resident_1d<double>(H, v.psis[0], dt, nsteps, st);
   }
   if (overlap_ok(v)) return run_rk4_overlapped(v, dt, nsteps, st);
-  if (v.hs.size() == 1 && !v.hs[0]->sharded && nsteps >= 4 && graph_ok()) return run_rk4_graph(v, dt, nsteps, st);
+  if (v.hs.size() == 1 && !v.hs[0]->sharded && nsteps >= 4 && v.hs[0]->opt_graph) return run_rk4_graph(v, dt, nsteps, st);
   for (int64_t n = 0; n < nsteps; ++n)
     for (int s = 1; s <= 4; ++s) {
       TRY(exchange(v, s, st));
@@ -1231,6 +1210,23 @@ nlse2shoc_status nlse2shoc_set_variant(nlse2shoc_t H, int variant) {
   for (nlse2shoc_t S : H->slabs) TRY(nlse2shoc_set_variant(S, variant));
   if ((variant == 1 || variant == 3) && H->slabs.empty()) TRY(ensure_D(H, variant == 3 ? H->dims : 1));
   H->variant = variant;
+  return NLSE2SHOC_OK;
+}
+
+nlse2shoc_status nlse2shoc_set_option(nlse2shoc_t H, int option, int64_t value) {
+  if (!H) return fail(NLSE2SHOC_EINVAL, "NULL handle");
+  if (value < 0 || value > (int64_t(1) << 30)) return fail(NLSE2SHOC_EINVAL, "option value out of range");
+  const int v = int(value);
+  switch (option) {
+    case NLSE2SHOC_OPT_CUDA_GRAPH: H->opt_graph = v != 0; break;
+    case NLSE2SHOC_OPT_OVERLAP: H->opt_overlap = v != 0; break;
+    case NLSE2SHOC_OPT_RESIDENT_1D: H->opt_resident = v != 0; break;
+    case NLSE2SHOC_OPT_REVERSE_ORDER: H->opt_reverse = v != 0; break;
+    case NLSE2SHOC_OPT_LEAN_STEPS: H->opt_lean = v & 3; break;
+    case NLSE2SHOC_OPT_ZCHUNKS: H->opt_zchunks = v; break;
+    default: return fail(NLSE2SHOC_EINVAL, "unknown option");
+  }
+  for (nlse2shoc_t S : H->slabs) TRY(nlse2shoc_set_option(S, option, value));
   return NLSE2SHOC_OK;
 }
 

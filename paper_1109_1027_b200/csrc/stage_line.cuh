@@ -171,12 +171,8 @@ __global__ void __launch_bounds__(256) line_tile_kernel(const cplx<R> *__restric
 // the grid are loaded with plain loads (out-of-range halo entries are never read: the two
 // points at each end go through line_point on global memory).  Same arithmetic as
 // line_tile_kernel.
-#ifndef NLSE_LS_SEG64
-#define NLSE_LS_SEG64 1024
-#define NLSE_LS_NS64 4
-#endif
 template <typename R> struct LineStream {
-  static constexpr int SEG = sizeof(R) == 4 ? NLSE_LS_SEG64 : 1024, NS = sizeof(R) == 4 ? NLSE_LS_NS64 : 3, NT = 256;
+  static constexpr int SEG = 1024, NS = sizeof(R) == 4 ? 4 : 3, NT = 256;
 };
 template <typename R, int MODE> __host__ __device__ constexpr int line_npa() {
   return MODE == M_S4X ? 3 : ((MODE == M_S4R || MODE == M_S2 || MODE == M_S3 || MODE == M_S4) ? 2 :

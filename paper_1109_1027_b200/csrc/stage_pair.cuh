@@ -31,33 +31,15 @@ enum PairKind { PAIR_A = 0, PAIR_B = 1 };
 // W_IN: input slot row (x0-4 ...), W_EX: mid / Psi-ext slot row (x0-2 ...); rings: RI input
 // planes (5 pinned + prefetch), 5 mid planes, RPS Psi-ext planes and RA acc tiles (pair B).
 template <int DIMS, typename R> struct PCfg;
-// 3D complex64 presets (NLSE_PAIR3F_PRESET; C4 768^3 ms per step, one B200):
-//   0 = 64 x 16 tiles, 8 consumer warps x 2 rows (168 registers)          18.5
-//   1 = 60 x 16 tiles, 15 consumer warps x 1 row (16 warps, 128 registers) 13.5  (default)
-//   2 = 48 x 20 tiles, 15 consumer warps x 1 row                            14.7
-// (the per-stage kernels take 9.9: see DESIGN.md §6 for why the pairs lose)
-#ifndef NLSE_PAIR3F_PRESET
-#define NLSE_PAIR3F_PRESET 1
-#endif
-#if NLSE_PAIR3F_PRESET == 2
-template <> struct PCfg<3, float> {
-  static constexpr int TX = 48, TY = 20, PPX = 2, RPW = 1, NCW = 15;
-  static constexpr int W_IN = 56, NBOX_IN = 1, W_EX = 52, NBOX_EX = 1, NBOXP = 1;
-  static constexpr int RI_A = 9, RI_B = 7, RPS = 4, RA = 2;
-};
-#elif NLSE_PAIR3F_PRESET == 1
+// 3D complex64 tiles: 60 x 16, 15 consumer warps x 1 row (16 warps, 128 registers).  Sweep
+// (C4 768^3 ms per step, one B200): 64 x 16 / 8 warps x 2 rows (168 registers) 18.5;
+// 60 x 16 / 15 x 1 13.5 (kept); 48 x 20 / 15 x 1 14.7.  The per-stage kernels take 8.8:
+// DESIGN.md §6 says why the pairs lose.
 template <> struct PCfg<3, float> {
   static constexpr int TX = 60, TY = 16, PPX = 2, RPW = 1, NCW = 15;
   static constexpr int W_IN = 68, NBOX_IN = 1, W_EX = 64, NBOX_EX = 1, NBOXP = 1;
   static constexpr int RI_A = 9, RI_B = 7, RPS = 4, RA = 2;
 };
-#else
-template <> struct PCfg<3, float> {
-  static constexpr int TX = 64, TY = 16, PPX = 2, RPW = 2, NCW = 8;
-  static constexpr int W_IN = 72, NBOX_IN = 1, W_EX = 68, NBOX_EX = 1, NBOXP = 1;
-  static constexpr int RI_A = 9, RI_B = 7, RPS = 4, RA = 2;
-};
-#endif
 template <> struct PCfg<3, double> {
   static constexpr int TX = 32, TY = 16, PPX = 1, RPW = 2, NCW = 8;
   static constexpr int W_IN = 40, NBOX_IN = 1, W_EX = 36, NBOX_EX = 1, NBOXP = 1;
@@ -115,13 +97,8 @@ __device__ __forceinline__ void sts_run(cplx<R> *p, const cplx<R> *v) {
   for (int i = 0; i < N / VV::CPV; ++i) reinterpret_cast<typename VV::T *>(p)[i] = VV::join(v + i * VV::CPV);
 }
 
-#ifdef NLSE_PAIR_MAXNREG
-#define NLSE_PAIR_BOUNDS(...) __maxnreg__(NLSE_PAIR_MAXNREG)
-#else
-#define NLSE_PAIR_BOUNDS(...) __launch_bounds__(__VA_ARGS__, 1)
-#endif
 template <int DIMS, typename R, int PAIR>
-__global__ void NLSE_PAIR_BOUNDS(PLayout<DIMS, R>::NTHREADS)
+__global__ void __launch_bounds__(PLayout<DIMS, R>::NTHREADS, 1)
     pair_stream_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_ps,
                        const __grid_constant__ CUtensorMap tm_acc, const StageParams<R> P) {
   using C = PCfg<DIMS, R>;
@@ -132,10 +109,7 @@ __global__ void NLSE_PAIR_BOUNDS(PLayout<DIMS, R>::NTHREADS)
   constexpr int RM = LY::RM, PPX = C::PPX, RPW = C::RPW, NT = C::NCW * 32;
   constexpr int RPSM = RPS > 0 ? RPS : 1, RAM = RA > 0 ? RA : 1;
   constexpr bool B = PAIR == PAIR_B;
-#ifndef NLSE_PAIR_AUNROLL
-#define NLSE_PAIR_AUNROLL 8
-#endif
-  constexpr int kAU = NLSE_PAIR_AUNROLL;  // unroll of phase A's task loop
+  constexpr int kAU = 8;  // unroll of phase A's task loop
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   CT *iring = reinterpret_cast<CT *>(smem_raw);
@@ -413,11 +387,7 @@ __global__ void NLSE_PAIR_BOUNDS(PLayout<DIMS, R>::NTHREADS)
           named_bar_sync(1, NT);
         }
       }
-#ifndef NLSE_PAIR_EXPT
-#define NLSE_PAIR_EXPT 0  // timing experiments only: 1 = skip phase A compute, 2 = skip phase B compute
-#endif
-      if (NLSE_PAIR_EXPT == 1) {
-      } else if (jin && leanA && gzj >= 2 && gzj <= NZ - 3) {
+      if (jin && leanA && gzj >= 2 && gzj <= NZ - 3) {
         const CT *s0 = islot(j), *sm1 = islot(j - 1), *sm2 = islot(j - 2), *sp1 = islot(j + 1), *sp2 = islot(j + 2);
         const CT *ps = B ? sslot(j) : nullptr;
         CT *md = mslot(j);
@@ -641,8 +611,7 @@ __global__ void NLSE_PAIR_BOUNDS(PLayout<DIMS, R>::NTHREADS)
           }
         }
         };
-        if (NLSE_PAIR_EXPT == 2) {
-        } else if (leanB && gz >= 2 && gz <= NZ - 3) bloop(std::true_type{});
+        if (leanB && gz >= 2 && gz <= NZ - 3) bloop(std::true_type{});
         else bloop(std::false_type{});
         outT += P.plane;
         if (!B) outA += P.plane;

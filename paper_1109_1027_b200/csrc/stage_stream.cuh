@@ -23,15 +23,7 @@
 #pragma once
 #include <type_traits>
 
-#ifndef NLSE_LEAN_DIMS
-#define NLSE_LEAN_DIMS 3
-#endif
-
 #include "common.cuh"
-
-#ifndef NLSE_ROW_BULK
-#define NLSE_ROW_BULK 1
-#endif
 
 namespace nlse {
 
@@ -56,23 +48,16 @@ enum Mode { M_S1 = 1, M_S2 = 2, M_S3 = 3, M_S4 = 4, M_LAP = 5, M_S1R = 6, M_S2R 
 template <int DIMS, typename R> struct Cfg;
 // Ring depths from a shared-memory budget: the T ring keeps the pinned window (planes
 // k-1..k+2) plus a prefetch depth, the P ring gets the rest.
-#ifndef NLSE_RING_BUDGET_KB
-#define NLSE_RING_BUDGET_KB 210
-#endif
-#ifndef NLSE_RT1_KB
-#define NLSE_RT1_KB 40
-#endif
-#ifndef NLSE_RT2_KB
-#define NLSE_RT2_KB 24
-#endif
+// (210 KB budget; T-ring prefetch 40 KB with one pointwise stream, 24 KB with two or three:
+// the depth sweep is in profiles/r01/README.md)
 template <int SLOT_B, int PT_B> struct Rings {
-  static constexpr int BUDGET = NLSE_RING_BUDGET_KB * 1024;
+  static constexpr int BUDGET = 210 * 1024, RT1_KB = 40, RT2_KB = 24;
   static constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
   static constexpr int mn(int a, int b) { return a < b ? a : b; }
   static constexpr int RT0 = mn(24, BUDGET / SLOT_B);
-  static constexpr int RT1 = 4 + cdiv(NLSE_RT1_KB * 1024, SLOT_B);
+  static constexpr int RT1 = 4 + cdiv(RT1_KB * 1024, SLOT_B);
   static constexpr int RP1 = mn(12, (BUDGET - RT1 * SLOT_B) / PT_B);
-  static constexpr int RT2 = 4 + cdiv(NLSE_RT2_KB * 1024, SLOT_B);
+  static constexpr int RT2 = 4 + cdiv(RT2_KB * 1024, SLOT_B);
   static constexpr int RP2 = mn(8, (BUDGET - RT2 * SLOT_B) / (2 * PT_B));
   static constexpr int RT3 = mn(RT2, (BUDGET - 6 * PT_B) / SLOT_B);  // keep >= 2 slots of 3 tiles
   static constexpr int RP3 = mn(8, (BUDGET - RT3 * SLOT_B) / (3 * PT_B));
@@ -82,58 +67,20 @@ template <int SLOT_B, int PT_B> struct Rings {
 // chosen by a sweep over (TY, warps, rows/warp) on C4 (scripts/sweep.py; 28 rows / 14 warps
 // until the exact-cancellation stencil R30 made the stage more issue-bound: v18 A/B C4
 // 4.864e10 (28/14) vs 4.895e10 (24/12) vs 4.799e10 (24 rows, 8 warps x 3 rows)).
-#ifndef NLSE3F_TY
-#define NLSE3F_TY 24
-#define NLSE3F_NCW 12
-#define NLSE3F_RPW 2
-#endif
-template <> struct Cfg<3, float> : Rings<68 * (NLSE3F_TY + 4) * 8, 64 * NLSE3F_TY * 8> {
-  static constexpr int TX = 64, TY = NLSE3F_TY, PPX = 2, RPW = NLSE3F_RPW, NCW = NLSE3F_NCW, NBOX = 1, NBOXP = 1,
-                       W = 68;
+template <> struct Cfg<3, float> : Rings<68 * (24 + 4) * 8, 64 * 24 * 8> {
+  static constexpr int TX = 64, TY = 24, PPX = 2, RPW = 2, NCW = 12, NBOX = 1, NBOXP = 1, W = 68;
 };
 // 3D complex128 tiles: 32 x 32, 8 consumer warps x 4 rows (sweep on C5W c128, ms/step:
 // 32x28/14 warps x 2 rows 4.38, 32x32/8x4 4.24, 32x40/10x4 4.25, 32x20/10x2 4.29, 32x24/12x2 4.32)
-#ifndef NLSE3D_TY
-#define NLSE3D_TY 32
-#define NLSE3D_NCW 8
-#define NLSE3D_RPW 4
-#endif
-template <> struct Cfg<3, double> : Rings<36 * (NLSE3D_TY + 4) * 16, 32 * NLSE3D_TY * 16> {
-  static constexpr int TX = 32, TY = NLSE3D_TY, PPX = 1, RPW = NLSE3D_RPW, NCW = NLSE3D_NCW, NBOX = 1, NBOXP = 1,
-                       W = 36;
+template <> struct Cfg<3, double> : Rings<36 * (32 + 4) * 16, 32 * 32 * 16> {
+  static constexpr int TX = 32, TY = 32, PPX = 1, RPW = 4, NCW = 8, NBOX = 1, NBOXP = 1, W = 36;
 };
 // 2D: the streamed axis is y and a "plane" is one row of TX + halo (slots split into
-// 128-byte-aligned TMA boxes of <= 256 eight-byte elements).  Presets (NLSE2D_PRESET, for
-// sweeps; C3 8192^2 ms/step c128 / c64 on one B200, profiles/r01/README.md):
-//   0 = 512 (c64) / 256 (c128)-wide rows, 8 consumer warps, deep rings   1.79 / 3.34
-//   1 = same tile, half-depth rings (2 CTAs/SM)                          1.78 / 3.31
-//   2 = 1024 / 512-wide rows, 4 / 2 points per thread  (default)         1.49 / 2.67
-//   3 = 1024 / 512-wide rows, 16 consumer warps                          1.47 / 2.69
-//   4, 5 = 2048 / 1024-wide rows (register spills)                       2.16, 1.78 / 3.48, 3.47
-//   6 = preset 2 with a shallower T ring                                 1.50 / 2.67
+// 128-byte-aligned TMA boxes of <= 256 eight-byte elements).  Row width chosen by a sweep
+// (C3 8192^2 ms/step c128 / c64 on one B200, profiles/r01/README.md): 512 / 256-wide rows
+// 1.79 / 3.34, 1024 / 512-wide rows with 4 / 2 points per thread 1.49 / 2.67 (kept), the
+// same with 16 consumer warps 1.47 / 2.69, 2048 / 1024-wide rows 2.16 / 3.48 (spills).
 // Wider rows amortise the per-row barrier round trip over more bytes.
-#ifndef NLSE2D_PRESET
-#define NLSE2D_PRESET 2
-#endif
-#if NLSE2D_PRESET == 0
-template <> struct Cfg<2, float> {
-  static constexpr int TX = 512, TY = 1, PPX = 2, RPW = 1, NCW = 8, NBOX = 3, NBOXP = 2, W = 528;
-  static constexpr int RT0 = 40, RT1 = 24, RP1 = 20, RT2 = 20, RP2 = 12, RT3 = 20, RP3 = 8;
-};
-template <> struct Cfg<2, double> {
-  static constexpr int TX = 256, TY = 1, PPX = 1, RPW = 1, NCW = 8, NBOX = 3, NBOXP = 2, W = 264;
-  static constexpr int RT0 = 40, RT1 = 24, RP1 = 20, RT2 = 20, RP2 = 12, RT3 = 20, RP3 = 8;
-};
-#elif NLSE2D_PRESET == 1
-template <> struct Cfg<2, float> {
-  static constexpr int TX = 512, TY = 1, PPX = 2, RPW = 1, NCW = 8, NBOX = 3, NBOXP = 2, W = 528;
-  static constexpr int RT0 = 20, RT1 = 12, RP1 = 10, RT2 = 10, RP2 = 6, RT3 = 10, RP3 = 4;
-};
-template <> struct Cfg<2, double> {
-  static constexpr int TX = 256, TY = 1, PPX = 1, RPW = 1, NCW = 8, NBOX = 3, NBOXP = 2, W = 264;
-  static constexpr int RT0 = 20, RT1 = 12, RP1 = 10, RT2 = 10, RP2 = 6, RT3 = 10, RP3 = 4;
-};
-#elif NLSE2D_PRESET == 2
 template <> struct Cfg<2, float> {
   static constexpr int TX = 1024, TY = 1, PPX = 4, RPW = 1, NCW = 8, NBOX = 5, NBOXP = 4, W = 1040;
   static constexpr int RT0 = 24, RT1 = 12, RP1 = 12, RT2 = 10, RP2 = 7, RT3 = 10, RP3 = 4;
@@ -142,43 +89,6 @@ template <> struct Cfg<2, double> {
   static constexpr int TX = 512, TY = 1, PPX = 2, RPW = 1, NCW = 8, NBOX = 5, NBOXP = 4, W = 520;
   static constexpr int RT0 = 24, RT1 = 12, RP1 = 12, RT2 = 10, RP2 = 7, RT3 = 10, RP3 = 4;
 };
-#elif NLSE2D_PRESET == 4
-template <> struct Cfg<2, float> {
-  static constexpr int TX = 2048, TY = 1, PPX = 8, RPW = 1, NCW = 8, NBOX = 10, NBOXP = 8, W = 2080;
-  static constexpr int RT0 = 12, RT1 = 6, RP1 = 6, RT2 = 6, RP2 = 3, RT3 = 6, RP3 = 2;
-};
-template <> struct Cfg<2, double> {
-  static constexpr int TX = 1024, TY = 1, PPX = 4, RPW = 1, NCW = 8, NBOX = 10, NBOXP = 8, W = 1040;
-  static constexpr int RT0 = 12, RT1 = 6, RP1 = 6, RT2 = 6, RP2 = 3, RT3 = 6, RP3 = 2;
-};
-#elif NLSE2D_PRESET == 5
-template <> struct Cfg<2, float> {
-  static constexpr int TX = 2048, TY = 1, PPX = 4, RPW = 1, NCW = 16, NBOX = 10, NBOXP = 8, W = 2080;
-  static constexpr int RT0 = 12, RT1 = 6, RP1 = 6, RT2 = 6, RP2 = 3, RT3 = 6, RP3 = 2;
-};
-template <> struct Cfg<2, double> {
-  static constexpr int TX = 1024, TY = 1, PPX = 2, RPW = 1, NCW = 16, NBOX = 10, NBOXP = 8, W = 1040;
-  static constexpr int RT0 = 12, RT1 = 6, RP1 = 6, RT2 = 6, RP2 = 3, RT3 = 6, RP3 = 2;
-};
-#elif NLSE2D_PRESET == 6
-template <> struct Cfg<2, float> {
-  static constexpr int TX = 1024, TY = 1, PPX = 4, RPW = 1, NCW = 8, NBOX = 5, NBOXP = 4, W = 1040;
-  static constexpr int RT0 = 24, RT1 = 14, RP1 = 10, RT2 = 12, RP2 = 6, RT3 = 12, RP3 = 4;
-};
-template <> struct Cfg<2, double> {
-  static constexpr int TX = 512, TY = 1, PPX = 2, RPW = 1, NCW = 8, NBOX = 5, NBOXP = 4, W = 520;
-  static constexpr int RT0 = 24, RT1 = 14, RP1 = 10, RT2 = 12, RP2 = 6, RT3 = 12, RP3 = 4;
-};
-#else
-template <> struct Cfg<2, float> {
-  static constexpr int TX = 1024, TY = 1, PPX = 2, RPW = 1, NCW = 16, NBOX = 5, NBOXP = 4, W = 1040;
-  static constexpr int RT0 = 24, RT1 = 12, RP1 = 12, RT2 = 10, RP2 = 7, RT3 = 10, RP3 = 4;
-};
-template <> struct Cfg<2, double> {
-  static constexpr int TX = 512, TY = 1, PPX = 1, RPW = 1, NCW = 16, NBOX = 5, NBOXP = 4, W = 520;
-  static constexpr int RT0 = 24, RT1 = 12, RP1 = 12, RT2 = 10, RP2 = 7, RT3 = 10, RP3 = 4;
-};
-#endif
 
 template <typename R> struct StageParams {
   int nx, ny, nz;        // local extents: x, y (1 in 2D), streamed axis (local slab)
@@ -197,6 +107,7 @@ template <typename R> struct StageParams {
   R ca, cb;              // stage-combine coefficients (acc, T)
   R cA;                  // phase-A coefficient of the stage-pair kernel (stage_pair.cuh)
   int rev;               // traverse the tiles in reverse order (alternate stages: L2 reuse)
+  int lean;              // lean plane steps: bit 1 interior tiles, bit 2 3D face tiles (else general)
   int zb, ze;            // local planes [zb, ze) this launch computes (edge / interior split)
   int bc;                // 0 Dirichlet, 1 Laplacian-zero, 2 MSD (1D line kernels only)
   int vkind;             // 0 none, 1 harmonic tables, 2 array
@@ -388,18 +299,8 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
       }
       // stencil-input planes are re-read (halos) by neighbouring tiles: keep them in L2;
       // Psi^n / acc tiles are read exactly once: evict first.
-#ifndef NLSE_TPOL
-#define NLSE_TPOL 2
-#endif
-#ifndef NLSE_PPOL
-#define NLSE_PPOL 1
-#endif
-      const uint64_t pol_keep = NLSE_TPOL == 2 ? policy_evict_last() : (NLSE_TPOL == 1 ? policy_evict_normal() : policy_evict_first());
-      const uint64_t pol_stream = NLSE_PPOL == 0 ? policy_evict_first() : policy_evict_normal();
-#ifndef NLSE_ACC_LOAD_FIRST
-#define NLSE_ACC_LOAD_FIRST 0
-#endif
-      const uint64_t pol_acc = NLSE_ACC_LOAD_FIRST ? policy_evict_first() : pol_stream;
+      const uint64_t pol_keep = policy_evict_last();
+      const uint64_t pol_stream = policy_evict_normal();
       uint32_t tcnt = 0, pcnt = 0;
       for (int t = blockIdx.x; t < P.ntiles; t += G) {
         const int tt = P.rev ? P.ntiles - 1 - t : t;  // reversed order: read the L2-resident tail first
@@ -418,7 +319,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
             mbar_arrive_expect_tx(&fullT[slot], LY::SLOT_BYTES);
             CT *dst = ring + size_t(slot) * LY::SLOT;
             // 2D interior row segment: one contiguous bulk copy instead of NBOX tensor boxes
-            if (DIMS == 2 && NLSE_ROW_BULK && m == &tm_T && P.in_T && x0 - 2 >= 0 && x0 - 2 + W <= P.nx) {
+            if (DIMS == 2 && m == &tm_T && P.in_T && x0 - 2 >= 0 && x0 - 2 + W <= P.nx) {
               bulk_load_hint(dst, P.in_T + int64_t(pz) * P.pitch + (x0 - 2), LY::SLOT_BYTES, &fullT[slot], pol_keep);
             } else
 #pragma unroll
@@ -445,17 +346,16 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
                                        : LY::template needs_t3<MODE>();
             if (!want) continue;
             const CUtensorMap *m = q == 0 ? &tm_psi : (q == 1 ? &tm_acc : &tm_t3);
-            if (DIMS == 2 && NLSE_ROW_BULK && P.in_P[q] && x0 + TX <= P.nx) {  // whole row segment
+            if (DIMS == 2 && P.in_P[q] && x0 + TX <= P.nx) {  // whole row segment
               bulk_load_hint(dst + (q == 0 ? 0 : (q == 1 ? ACC_OFF : T3_OFF)), P.in_P[q] + int64_t(k) * P.pitch + x0,
-                             LY::PTILE_BYTES, &fullP[slot], q == 1 ? pol_acc : pol_stream);
+                             LY::PTILE_BYTES, &fullP[slot], pol_stream);
               continue;
             }
 #pragma unroll
             for (int b = 0; b < C::NBOXP; ++b) {
               const int c0 = x0 * LY::EPC + b * LY::BWP;
               char *d = reinterpret_cast<char *>(dst + (q == 0 ? 0 : (q == 1 ? ACC_OFF : T3_OFF))) + b * LY::BWP * 8;
-              // Psi^n is re-read by the next stage (L2 reuse); acc is not
-              const uint64_t pol = q == 1 ? pol_acc : pol_stream;
+              const uint64_t pol = pol_stream;
               if (DIMS == 3) tma_load_3d_hint(d, m, &fullP[slot], c0, y0, k, pol);
               else tma_load_2d_hint(d, m, &fullP[slot], c0, k, pol);
             }
@@ -727,7 +627,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
 #pragma unroll
           for (int v = 0; v < PPX / VV::CPV; ++v) {
             st_stream(reinterpret_cast<typename VV::T *>(oTr) + v, VV::join(oT + v * VV::CPV));
-            if (LY::template writes_acc<MODE>()) st_acc(reinterpret_cast<typename VV::T *>(oAr) + v, VV::join(oA + v * VV::CPV));
+            if (LY::template writes_acc<MODE>()) st_stream(reinterpret_cast<typename VV::T *>(oAr) + v, VV::join(oA + v * VV::CPV));
           }
         } else {
 #pragma unroll
@@ -890,7 +790,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
         for (int v = 0; v < PPX / VV::CPV; ++v) {
           st_stream(reinterpret_cast<typename VV::T *>(outT + r * pitch) + v, VV::join(oT + v * VV::CPV));
           if (LY::template writes_acc<MODE>())
-            st_acc(reinterpret_cast<typename VV::T *>(outA + r * pitch) + v, VV::join(oA + v * VV::CPV));
+            st_stream(reinterpret_cast<typename VV::T *>(outA + r * pitch) + v, VV::join(oA + v * VV::CPV));
         }
 #pragma unroll
         for (int q = 0; q < PPX; ++q) {
@@ -914,36 +814,22 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
       ph2 ^= sk2 == 0;
     };
 
-#ifndef NLSE_NO_LEAN
-#define NLSE_LEAN_OK true
-#else
-#define NLSE_LEAN_OK false
-#endif
-#ifndef NLSE_XFACE_LEAN
-#define NLSE_XFACE_LEAN 1
-#endif
     // face tiles (3D, full in x and y, separable V): the lean step plus the x/y-face ghost fill
     // and the face rule on the boundary columns/rows; bit-identical to the general step
-    const bool xface_lean = NLSE_XFACE_LEAN && NLSE_LEAN_OK && DIMS == 3 && !inner_xy && P.vkind != 2 &&
-                            x0 + TX <= nx && y0 + TY <= ny;
-    if (inner_xy && NLSE_LEAN_OK && (NLSE_LEAN_DIMS & DIMS)) {
+    // (P.lean bit 1: interior tiles, bit 2: face tiles; nlse2shoc_set_option LEAN_STEPS)
+    const bool face_lean = (P.lean & 2) && DIMS == 3 && !inner_xy && P.vkind != 2 && x0 + TX <= nx && y0 + TY <= ny;
+    if (inner_xy && (P.lean & 1)) {
       // lean planes: gz in [2, NZ-3], clamped to this tile's chunk [kb, ke)
       const int l0 = min(ke, max(kb, 2 - z0)), l1 = max(l0, min(ke, NZ - 2 - z0));
       int k = kb;
       for (; k < l0; ++k) general_step(k);
-#ifndef NLSE_LEAN_UNROLL
-#define NLSE_LEAN_UNROLL 1
-#endif
-      constexpr int kLU = NLSE_LEAN_UNROLL;
       if (P.vkind == 2) {
-#pragma unroll (kLU)
         for (; k < l1; ++k) lean_step(k, std::true_type{}, std::false_type{});
       } else {
-#pragma unroll (kLU)
         for (; k < l1; ++k) lean_step(k, std::false_type{}, std::false_type{});
       }
       for (; k < ke; ++k) general_step(k);
-    } else if (DIMS == 3 && xface_lean) {
+    } else if (DIMS == 3 && face_lean) {
       if constexpr (DIMS == 3) {
         const int l0 = min(ke, max(kb, 2 - z0)), l1 = max(l0, min(ke, NZ - 2 - z0));
         int k = kb;

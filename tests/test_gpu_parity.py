@@ -324,12 +324,13 @@ def test_C5W_full_size_crops(dtype):
 
 
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
-def test_1d_multilaunch_path_small_grid(dtype, monkeypatch):
+def test_1d_multilaunch_path_small_grid(dtype):
     """Small 1D grids normally run on the resident single-CTA solver; force the per-stage
     launch path (used for large 1D grids such as C2) and check parity on a small grid."""
-    monkeypatch.setenv("NLSE_NO_RESIDENT", "1")
     w = _small(1, (1001,), "dirichlet", dtype, "harmonic")
     S = H.gpu_solver(w, dtype)
+    S.set_option("resident_1d", 0)
+    S.set_option("cuda_graph", 0)
     psi = H.psi0_host(w, dtype)
     P = H.oracle_problem(w)
     dt = 0.8 * oracle.kmax(P, psi.astype(np.complex128))
@@ -456,3 +457,80 @@ def test_1d_stream_kernel_msd():
     ref = oracle.rk4(P, psi, dt, 20)
     assert np.isfinite(ref).all()
     assert H.rel_l2(g.cpu().numpy(), ref) <= 1e-12
+
+
+# ------------------------------------------------------------- execution-path options
+def _ragged_cases():
+    out = []
+    for dtype, TX, TY in (("c64", 64, 24), ("c128", 32, 32)):
+        for i, (dx, dy) in enumerate([(-1, 1), (1, -1), (0, 0)]):
+            out.append((dtype, (2 * TX + dx, 2 * TY + dy, 13), ("dirichlet", "lapzero")[i % 2]))
+    return out
+
+
+@pytest.mark.parametrize("variant", [0, 2, 6])
+@pytest.mark.parametrize("dtype,n,bc", _ragged_cases())
+def test_lean_steps_bit_identical_to_general_step(dtype, n, bc, variant):
+    """The lean plane steps (interior tiles, and 3D tiles touching an x/y face with the ghost
+    fill and face rule inline) evaluate the general step's expressions: forcing the general
+    step everywhere (option LEAN_STEPS = 0) must give the same bits, for every RK4 stage kind
+    and the Laplacian, on grids one point either side of two-tile multiples."""
+    w = _small(3, n, bc, dtype, "harmonic")
+    psi = H.psi0_host(w, dtype)
+    dt = 0.8 * oracle.kmax(H.oracle_problem(w), psi.astype(np.complex128))
+    outs, laps = [], []
+    for lean in (3, 2, 1, 0):
+        S = H.gpu_solver(w, dtype, variant)
+        S.set_option("lean_steps", lean)
+        g = _dev(psi)
+        S.rk4(g, dt, 3)
+        outs.append(g.cpu())
+        laps.append(S.laplacian(_dev(psi)).cpu())
+    for o, l in zip(outs[1:], laps[1:]):
+        assert torch.equal(o, outs[0])
+        assert torch.equal(l, laps[0])
+
+
+@pytest.mark.parametrize("nz,chunks", [(33, 8), (33, 5), (40, 3), (9, 50)])
+def test_zchunk_counts_bit_identical(nz, chunks):
+    """z-chunking only changes which CTA computes a plane: any chunk count (including ones
+    that would leave empty chunks, which are normalised) gives the same bits."""
+    w = _small(3, (70, 30, nz), "dirichlet", "c64", "harmonic")
+    psi = H.psi0_host(w, "c64")
+    ref = None
+    for c in (0, chunks):
+        S = H.gpu_solver(w, "c64")
+        S.set_option("zchunks", c)
+        g = _dev(psi)
+        S.rk4(g, 1e-4, 2)
+        if ref is None:
+            ref = g.cpu()
+        else:
+            assert torch.equal(g.cpu(), ref)
+
+
+@pytest.mark.parametrize("option", ["cuda_graph", "reverse_order"])
+def test_path_options_bit_identical(option):
+    w = _small(3, (70, 30, 20), "lapzero", "c64", "harmonic")
+    psi = H.psi0_host(w, "c64")
+    res = []
+    for v in (1, 0):
+        S = H.gpu_solver(w, "c64")
+        S.set_option(option, v)
+        g = _dev(psi)
+        S.rk4(g, 1e-4, 5)
+        res.append(g.cpu())
+    assert torch.equal(res[0], res[1])
+
+
+def test_V_array_is_validated():
+    """the array potential reaches the library as a raw pointer; the binding must
+    refuse a tensor the kernels would read out of bounds or in the wrong precision."""
+    w = _small(3, (9, 8, 7), "dirichlet", "c128", "array")
+    good = H.V_array_device(w, "c128")
+    import paper_1109_1027_b200 as nl
+
+    for bad in (good.float(), good[:-1].clone(), good.cpu(), good.reshape(7, 8, 9).transpose(0, 2)):
+        with pytest.raises(ValueError):
+            nl.solver_from_work(w, "c128", V_array=bad)
+    nl.solver_from_work(w, "c128", V_array=good).close()

@@ -478,3 +478,91 @@ def test_P6_fig1_orders():
     assert abs(metrics.order(e[0.25], e[0.125], 0.25, 0.125) - 3.9788) < 5e-3
     c = {h: run_exp1(h, "cd")[0] for h in (0.5, 0.25)}
     assert abs(metrics.order(c[0.5], c[0.25], 0.5, 0.25) - 2.0352) < 5e-3
+
+
+# ------------------------------------------------------------ kdfull with N != 0 (a8)
+def _operator_matrix(P, shape):
+    """Brute force: the matrix of F/i = a Lap + N on the interior unknowns (Psi_b = 0),
+    one oracle RHS evaluation per unit vector."""
+    I = interior(len(shape), shape)
+    idx = np.argwhere(np.ones(tuple(n - 2 for n in shape), bool)) + 1
+    M = np.zeros((len(idx), len(idx)))
+    for q, ii in enumerate(idx):
+        e = np.zeros(shape, complex)
+        e[tuple(ii)] = 1.0
+        M[:, q] = (oracle.rhs(P, e)[I] / 1j).reshape(-1).real
+    return M
+
+
+@pytest.mark.parametrize("dims,hs,vext", [
+    (2, [0.3, 0.3], 0.0), (2, [0.3, 0.41], 0.0), (2, [0.3, 0.3], -200.0), (2, [0.3, 0.41], -200.0),
+    (1, [0.2], 0.0), (1, [0.2], -400.0), (3, [0.5, 0.5, 0.5], 0.0), (3, [0.5, 0.6, 0.7], -80.0)])
+def test_kdfull_equals_brute_force_gershgorin(dims, hs, vext):
+    """`kdfull` (P:446-455) with N != 0: k_max = sqrt(8) / max_i (|M_ii| + sum_{j!=i} |M_ij|),
+    the Gershgorin bound of the operator's own matrix built point by point.  The extremes of
+    N are placed on depth >= 3 rows (no neighbour on the boundary, so their discs are the
+    widest, Table 2's 30 +- 34 class),
+    one far below and (vext != 0) one far above the rest, so that each of the two branches
+    max(g_max - L_min, L_max - g_min) decides in one of the cases: a swapped L_min / L_max, a
+    wrong G endpoint or a missing h^2/a factor changes k_max by far more than 1e-12.  The
+    anisotropic cases pin reading R17's per-axis Gershgorin sum the same way."""
+    n = 9
+    shape = (n,) * dims
+    rng = np.random.default_rng(17 + dims)
+    V = rng.uniform(-3, 3, shape)
+    c = (n // 2,) * dims
+    V[c] = 40.0                        # N = -V: the minimum of N, at a depth-4 point
+    if vext:
+        V[(3,) * dims] = vext          # far above, depth 3: Nmax + (4/12) a H decides
+    a = 0.8
+    P = oracle.Problem(dims, [n] * dims, hs, a, 0.0, V, "dirichlet")
+    M = _operator_matrix(P, shape)
+    gersh = max(abs(M[i, i]) + np.abs(M[i]).sum() - abs(M[i, i]) for i in range(M.shape[0]))
+    k = oracle.kmax(P, np.zeros(shape, complex))
+    assert abs(k - math.sqrt(8) / gersh) <= 1e-12 * k
+    # which branch decided (documents that both are exercised)
+    Hs = sum(1 / h ** 2 for h in hs)
+    nmin, nmax = float(-V.max()), float(-V.min())
+    lo_branch = 64 / 12 * a * Hs - nmin
+    hi_branch = nmax + 4 / 12 * a * Hs
+    assert (hi_branch > lo_branch) == (vext != 0)
+
+
+# survey §8(d): k_max of C1-C5 at t = 0, derived there independently (numpy) from Psi0's
+# extremes; printed to 7 significant digits, so the tolerance is half a unit of the last one.
+KMAX_SURVEY = {"C1": 8.108023e-4, "C2": 4.823326e-9, "C3": 4.551916e-6, "C4": 1.530532e-4, "C5": 4.419417e-4}
+
+
+def _kmax_full(work, dtype="c128", slab=32):
+    g = work["grid"]
+    dims = g["dims"]
+    lo_all, hi_all = np.inf, -np.inf
+    for z0 in range(0, g["n"][dims - 1], slab):
+        lo = [0, 0, 0]
+        cnt = list(g["n"])
+        lo[dims - 1] = z0
+        cnt[dims - 1] = min(slab, g["n"][dims - 1] - z0)
+        psi = icgen.fill(work["ic"], g, dtype=np.complex64 if dtype == "c64" else np.complex128, lo=lo, cnt=cnt)
+        a, b = oracle.N_minmax(oracle.problem_from_work(work, lo=lo, cnt=cnt), psi.astype(np.complex128))
+        lo_all, hi_all = min(lo_all, a), max(hi_all, b)
+    return oracle.kmax_from_N(dims, g["h"][:dims], work["a"], lo_all, hi_all), lo_all, hi_all
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_kmax_of_the_configs_matches_survey(name):
+    """The oracle's k_max on each config's full grid (C5: the weak-scaling grid of one GPU,
+    whose k_max the survey states equal to the 1536^3 grid's: L_min ~ 0 and g_max decide)."""
+    work = {"C1": configs.C1, "C2": configs.C2, "C3": configs.C3, "C4": configs.C4,
+            "C5": lambda: configs.C5W(1)}[name]()
+    k, nmin, nmax = _kmax_full(work, "c64" if name == "C4" else "c128")
+    want = KMAX_SURVEY[name]
+    assert abs(k - want) <= 0.5e-6 * want * 1.0001, (k, want)
+    # the pin discriminates: the bound with L_min and L_max exchanged in the two branches
+    # (max(g_max - L_max, L_min - g_min)) lies outside the printed digits (except C2, where
+    # h^2 |Psi|^2 ~ 1e-8 is below them)
+    if name != "C2":
+        g = work["grid"]
+        d, hh, a = g["dims"], g["h"][0] ** 2, work["a"]
+        Lmin, Lmax = hh / a * nmin, hh / a * nmax
+        kswap = math.sqrt(8) / max(64 * d / 12 - Lmax, Lmin + 4 * d / 12) * hh / a
+        assert abs(kswap - want) > 0.5e-6 * want
