@@ -1,12 +1,16 @@
 #!/usr/bin/env python
 """Benchmark: grid-point RK4 steps/s of the 2SHOC NLSE step (BASELINE.json metric).
 
-Workload (N=1): C4 — 3D vortex ring, 768^3, complex64, Dirichlet, V = r^2/2 (BASELINE.json
-configs[3]), the configuration the north star's >=70%-of-roofline target binds.  One bench
-"step" = one full RK4 step (4 fused stage launches) over the whole grid.  N>1: the same
-768^3 grid z-slab sharded over N ranks (strong scaling, per-stage 2-plane NCCL halo).
+Workload (default, N=1): C4 — 3D vortex ring, 768^3, complex64, Dirichlet, V = r^2/2
+(BASELINE.json configs[3]), the configuration the north star's >=70%-of-roofline target
+binds.  One bench "step" = one full RK4 step (4 fused stage launches) over the whole grid.
+N>1: the same 768^3 grid z-slab sharded over N ranks (strong scaling, per-stage 2-plane NCCL
+halo).  --workload C5W: the weak-scaling config (768 x 768 x 192 per GPU, 768 x 768 x 192N
+in all, Laplacian-zero Gaussian, BASELINE configs[4]); C5S (1536^3, strong), C3 (8192^2
+c128) and C2 (2^22, 1D) are the other parity configs, for the perf table.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload C4|C5W|C5S|C3|C2] [--dtype c64|c128]
 
 Timing: W untimed warm-up steps, then K steps inside one nlse2shoc_rk4 call bracketed by a
 barrier + cuda synchronize, CUDA events on the launching stream, max over ranks.  Every
@@ -27,7 +31,23 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "grid-point RK4 steps/s (2SHOC NLSE)"
+WORKLOADS = {"C4": "C4_vortex_ring_3d (BASELINE configs[3])",
+             "C5W": "C5W_gaussian_3d weak scaling 768x768x192 per GPU (BASELINE configs[4])",
+             "C5S": "C5S_gaussian_3d 1536^3 (BASELINE configs[4])",
+             "C3": "C3_vortex_lattice_2d 8192^2 (BASELINE configs[2])",
+             "C2": "C2_dark_soliton_1d 2^22 (BASELINE configs[1])"}
+KERNEL = {3: "stage_stream_kernel<3,{},*> (avg over the 4 stage launches)",
+          2: "stage_stream_kernel<2,{},*> (avg over the 4 stage launches)",
+          1: "line kernels <{}> (avg over the 4 stage launches)"}
 UNIT = "pt-steps/s"
+DTYPE_DEFAULT = {"C3": "c128", "C2": "c128"}
+
+
+def workload(wl, ws):
+    from icgen import configs
+
+    return {"C4": configs.C4, "C5W": lambda: configs.C5W(ws), "C5S": configs.C5, "C3": configs.C3,
+            "C2": configs.C2}[wl]()
 
 
 def dist_env():
@@ -102,8 +122,9 @@ class Clocks:
         return {"sm_mhz": statistics.median(sms), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sms)}
 
 
-def oracle_sample(work, steps_per_call, box=96):
-    """Time the CPU oracle on a centred box of the workload (bounded sample)."""
+def oracle_sample(work, steps_per_call, box=96, dtype="c64"):
+    """Time the CPU oracle on a centred box of the workload (bounded sample; box = edge length
+    in 3D, scaled to the same point count in 2D / 1D)."""
     import numpy as np
 
     import icgen
@@ -111,16 +132,19 @@ def oracle_sample(work, steps_per_call, box=96):
 
     g = work["grid"]
     n = g["n"]
+    box = int(round(box ** (3.0 / g["dims"])))
     lo = [max(0, (n[d] - box) // 2) if d < g["dims"] else 0 for d in range(3)]
     cnt = [min(box, n[d]) if d < g["dims"] else 1 for d in range(3)]
-    psi = icgen.fill(work["ic"], g, dtype=np.complex64, lo=lo, cnt=cnt).astype(np.complex128)
+    psi = icgen.fill(work["ic"], g, dtype=np.complex64 if dtype == "c64" else np.complex128, lo=lo,
+                     cnt=cnt).astype(np.complex128)
     P = oracle.problem_from_work(work, lo=lo, cnt=cnt)
     dt = 0.8 * oracle.kmax(P, psi)
     t0 = time.perf_counter()
     oracle.rk4(P, psi, dt, steps_per_call)
     t = time.perf_counter() - t0
     pts = int(np.prod([cnt[d] for d in range(g["dims"])]))
-    return pts, t, f"C4 centred {'x'.join(str(c) for c in cnt[:g['dims']])} box, {steps_per_call} RK4 step(s), oracle in double"
+    name = work["name"].split("_")[0]
+    return pts, t, f"{name} centred {'x'.join(str(c) for c in cnt[:g['dims']])} box, {steps_per_call} RK4 step(s), oracle in double"
 
 
 def cores():
@@ -167,23 +191,23 @@ def run_reference(args):
             dist.barrier()
             dist.destroy_process_group()
             return
-    from icgen import configs
-
-    work = configs.C4()
+    wl = args.workload
+    work = workload(wl, ws)
+    dtype = args.dtype or DTYPE_DEFAULT.get(wl, "c64")
     box = int(os.environ.get("NLSE_REF_BOX", "96"))
     for _ in range(args.warmup):
-        oracle_sample(work, 1, box=min(box, 48))
+        oracle_sample(work, 1, box=min(box, 48), dtype=dtype)
     tot_pts, tot_t, desc = 0, 0.0, ""
     for _ in range(args.steps):
-        pts, t, desc = oracle_sample(work, 1, box=box)
+        pts, t, desc = oracle_sample(work, 1, box=box, dtype=dtype)
         tot_pts += pts
         tot_t += t
     value = tot_pts / tot_t
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference",
-            "config": {"workload": "C4_vortex_ring_3d (BASELINE configs[3]) sample", "grid": [768, 768, 768],
+            "scaling": "weak" if wl == "C5W" else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": WORKLOADS[wl] + " sample", "grid": work["grid"]["n"][:work["grid"]["dims"]],
                        "sample": desc},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores(), "kind": "oracle", "sample": desc,
                              **host_info()},
@@ -219,16 +243,24 @@ def run_ours(args):
 
     import icgen
 
-    work = configs.C4()
-    dtype = "c64"
+    wl = args.workload
+    work = workload(wl, ws)
+    dtype = args.dtype or DTYPE_DEFAULT.get(wl, "c64")
+    if work["grid"]["dims"] == 1 and ws > 1:
+        raise SystemExit("1D configs are replicas only (DESIGN.md §8): run --gpus 1")
     S = nl.solver_from_work(work, dtype, shard=shard)
+    ctype = torch.complex64 if dtype == "c64" else torch.complex128
     g = work["grid"]
     npts_global = int(np.prod(g["n"][:3]))
     lshape = S.local_shape
-    lo = [0, 0, S.z0]
-    cnt = [g["n"][0], g["n"][1], S.nz]
-    host = torch.empty(lshape, dtype=torch.complex64, pin_memory=True)
-    icgen.fill(work["ic"], g, dtype=np.complex64, lo=lo, cnt=cnt, out=host.numpy())
+    dims = g["dims"]
+    lo = [0, 0, 0]
+    cnt = list(g["n"])
+    if dims >= 2:
+        lo[dims - 1], cnt[dims - 1] = S.z0, S.nz
+    host = torch.empty(lshape, dtype=ctype, pin_memory=True)
+    icgen.fill(work["ic"], g, dtype=np.complex64 if dtype == "c64" else np.complex128, lo=lo, cnt=cnt,
+               out=host.numpy())
     psi = host.cuda()
     kmax = S.stability_bound(psi)
     dt = 0.8 * kmax
@@ -261,7 +293,7 @@ def run_ours(args):
     value = npts_global * args.steps / (ms / 1e3)
 
     # end-to-end through the public API with HOST buffers: H2D(Psi0) + rk4(K) + D2H(Psi)
-    out_host = torch.empty(lshape, dtype=torch.complex64, pin_memory=True)  # empty_like would not pin
+    out_host = torch.empty(lshape, dtype=ctype, pin_memory=True)  # empty_like would not pin
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     torch.cuda.synchronize()
@@ -278,43 +310,50 @@ def run_ours(args):
     ems = float(te.item())
     nbytes = host.numel() * host.element_size() * ws
 
-    S_bytes = 8
-    # the fused default's own minimum traffic: 13 complex transfers per point-step
-    # (write-light form, stages 2 / 3 / 3 / 5); SURVEY §8(d) counts 16 for the
-    # explicit-accumulator form, reported beside it as achieved_16S_equiv
-    transfers = 13
-    alg_bytes_per_launch = transfers / 4 * S_bytes * npts_global / ws
-    launch_ms = ms / (4 * args.steps)
-    achieved = alg_bytes_per_launch / (launch_ms / 1e3) / 1e9
+    S_bytes = 8 if dtype == "c64" else 16
+    # Roofline: the algorithmic bytes are 16 S per point-step (the minimum with
+    # every stage result stored); the fused default moves 13 S (write-light form),
+    # so its 16 S rate can exceed the copy bandwidth.  Reported beside it: the 13 S rate and
+    # the DRAM-counter rate (ncu bytes of the same kernels, profiles/roofline_traffic.json).
+    pts_local = npts_global / ws
+    launch_ms = ms / (4 * args.steps)  # the 4 stage launches of a step (device time per launch)
+    achieved = 16 / 4 * S_bytes * pts_local / (launch_ms / 1e3) / 1e9
     peak, peak_kind = peaks()
     tr = profile_traffic()
     traffic = None
-    if tr and tr.get("workload") == "C4" and tr.get("dram_bytes_per_point_stage"):
-        traffic = tr["dram_bytes_per_point_stage"] * npts_global / ws
+    key = f"{wl}_{dtype}"
+    if tr and tr.get("workload") in (wl, key) and tr.get("dram_bytes_per_point_stage"):
+        traffic = tr["dram_bytes_per_point_stage"] * pts_local
     clocks = clk.summary()
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "c64 (fp32 pairs)", "data": "synthetic",
-            "config": {"workload": "C4_vortex_ring_3d (BASELINE configs[3])", "grid": g["n"][:3],
-                       "bc": "dirichlet", "V": "harmonic 0.5 r^2", "dt": dt, "kmax": kmax,
+            "scaling": "weak" if wl == "C5W" else "strong", "vs_baseline": None,
+            "dtype": "c64 (fp32 pairs)" if dtype == "c64" else "c128 (fp64 pairs)", "data": "synthetic",
+            "config": {"workload": WORKLOADS[wl], "grid": g["n"][:dims], "bc": work["bc"],
+                       "V": work["V"]["kind"], "dt": dt, "kmax": kmax,
                        "parallelism": f"z-slab x{ws}" if ws > 1 else "single GPU",
-                       "l2": "inputs (3.4 GiB per field) >> L2 (126 MB); no flush"},
+                       "l2": f"inputs ({host.numel() * host.element_size() / 2**30:.2f} GiB per field per GPU) vs "
+                             "L2 126 MB: no flush" + (" (C2: fields comparable to L2, DRAM bytes can fall "
+                                                      "below algorithmic)" if wl == "C2" else "")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "alg_bytes_per_point_step": transfers * S_bytes,
-                         "achieved_16S_equiv": achieved * 16 / transfers,
+                         "alg_bytes_per_point_step": 16 * S_bytes,
+                         "alg_bytes_note": "SURVEY 8(d) 16 S per point-step; the write-light default moves 13 S",
+                         "achieved_13S": achieved * 13 / 16, "frac_13S": achieved * 13 / 16 / peak,
+                         "dram_achieved": (traffic / (launch_ms / 1e3) / 1e9) if traffic else None,
+                         "dram_frac": (traffic / (launch_ms / 1e3) / 1e9 / peak) if traffic else None,
                          "frac_of_8TBs": achieved / 8000.0,
-                         "kernel": "stage_stream_kernel<3,float,*> (avg over the 4 stage launches)"},
+                         "kernel": KERNEL[dims].format("float" if dtype == "c64" else "double")},
             "e2e": {"value": npts_global * args.steps / (ems / 1e3), "unit": UNIT,
                     "h2d_bytes_per_step": nbytes / args.steps, "d2h_bytes_per_step": nbytes / args.steps,
                     "note": "per job of K steps: H2D(Psi0 pinned) + nlse2shoc_rk4(K) + D2H(Psi)"},
             "gpu_launches": launches,
             "clocks": clocks,
         }
-        if ws == 1 and not args.no_cpu_baseline:
+        if ws == 1 and not args.no_cpu_baseline and wl == "C4":
             line["cpu_baseline"] = cpu_baseline_line(work, int(os.environ.get("NLSE_REF_BOX", "96")))
         print(json.dumps(line), flush=True)
     S.close()
@@ -330,6 +369,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="C4", choices=["C4", "C5W", "C5S", "C3", "C2"])
+    ap.add_argument("--dtype", default=None, choices=["c64", "c128"])
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

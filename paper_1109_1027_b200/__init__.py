@@ -119,7 +119,8 @@ def nlse2shoc_check_finite(H, psi, stream=None):
     check(lib().nlse2shoc_check_finite(H, _ptr(psi), _stream(stream)), "check_finite")
 
 
-OPTIONS = {"cuda_graph": 0, "overlap": 1, "resident_1d": 2, "reverse_order": 3, "lean_steps": 4, "zchunks": 5}
+OPTIONS = {"cuda_graph": 0, "overlap": 1, "resident_1d": 2, "reverse_order": 3, "lean_steps": 4, "zchunks": 5,
+           "tile_schedule": 6}
 
 
 def nlse2shoc_set_option(H, option, value: int):
@@ -186,7 +187,7 @@ class Solver:
 
     def set_option(self, option, value: int):
         """Execution-path option (include/nlse2shoc.h nlse2shoc_option): 'cuda_graph',
-        'overlap', 'resident_1d', 'reverse_order', 'lean_steps', 'zchunks'."""
+        'overlap', 'resident_1d', 'reverse_order', 'lean_steps', 'zchunks', 'tile_schedule'."""
         nlse2shoc_set_option(self._h, option, value)
 
     def set_scheme(self, scheme):

@@ -111,6 +111,16 @@ struct nlse2shoc_s {
   // execution-path options (nlse2shoc_set_option): results are the same up to the rounding
   // differences stated in include/nlse2shoc.h
   int opt_graph = 1, opt_overlap = 1, opt_resident = 1, opt_reverse = 1, opt_lean = 3, opt_zchunks = 0;
+  int opt_sched = -1;         // -1: automatic (dynamic in 3D, static in 2D)
+  unsigned *sched = nullptr;  // dynamic tile schedule counters {next tile, finished CTAs}
+  // one instantiated RK4-step graph, reused by later calls with the same psi, dt and settings
+  // (gen counts set_variant / set_scheme / set_option calls)
+  cudaGraphExec_t gexec = nullptr;
+  const void *g_psi = nullptr;
+  double g_dt = 0.0;
+  int g_kind = 0;
+  uint64_t gen = 0, g_gen = 0;
+  int64_t g_launches = 0;
   // loopback (single-GPU emulation of z-slab sharding, SURVEY §4 T3'): virtual slabs that
   // exchange halos by device copies instead of NCCL; empty for ordinary handles
   std::vector<nlse2shoc_s *> slabs;
@@ -266,6 +276,7 @@ template <typename R> static void fill_params(nlse2shoc_t H, StageParams<R> &P) 
   P.inv_a = R(1.0 / H->a);
   P.bc = H->bc;
   P.lean = H->opt_lean;
+  P.sched = (H->opt_sched < 0 ? H->dims == 3 : H->opt_sched != 0) ? H->sched : nullptr;
   P.vkind = int(H->V.kind);
   if (H->V.kind == NLSE2SHOC_V_HARMONIC) {
     const R *t = reinterpret_cast<const R *>(H->vtab);
@@ -702,6 +713,78 @@ static nlse2shoc_status stage_range(nlse2shoc_t H, Field &psi, int s, double dt,
   return r;
 }
 
+// Graph cache: the last instantiated step graph of a handle, valid for the same stencil-input
+// base pointer, dt, kind and settings generation.
+static bool graph_cached(nlse2shoc_t H, const void *psi, double dt, int kind) {
+  return H->gexec && H->g_psi == psi && H->g_dt == dt && H->g_kind == kind && H->g_gen == H->gen;
+}
+static void graph_drop(nlse2shoc_t H) {
+  if (H->gexec) cudaGraphExecDestroy(H->gexec);  // deferred by the driver until pending launches end
+  H->gexec = nullptr;
+  H->g_kind = 0;
+}
+static nlse2shoc_status graph_replay(nlse2shoc_t H, int64_t nsteps, cudaStream_t st) {
+  cudaError_t el = cudaSuccess;
+  for (int64_t n = 0; n < nsteps && el == cudaSuccess; ++n) el = cudaGraphLaunch(H->gexec, st);
+  if (el != cudaSuccess) return fail(NLSE2SHOC_ECUDA, std::string("graph launch: ") + cudaGetErrorString(el));
+  return NLSE2SHOC_OK;
+}
+// End the capture on cs, instantiate and remember the graph in H.
+static nlse2shoc_status graph_finish(nlse2shoc_t H, cudaStream_t cs, nlse2shoc_status r, const void *psi, double dt,
+                                     int kind) {
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(cs, &graph);
+  if (r != NLSE2SHOC_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return r;
+  }
+  if (ec != cudaSuccess) return fail(NLSE2SHOC_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ec));
+  graph_drop(H);
+  const cudaError_t ei = cudaGraphInstantiate(&H->gexec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ei != cudaSuccess) {
+    H->gexec = nullptr;
+    return fail(NLSE2SHOC_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei));
+  }
+  H->g_psi = psi;
+  H->g_dt = dt;
+  H->g_kind = kind;
+  H->g_gen = H->gen;
+  return NLSE2SHOC_OK;
+}
+
+// One RK4 step of the edge-first schedule, enqueued on st (the side stream joins and rejoins
+// st through events, so the whole step can be captured in a CUDA graph).
+static nlse2shoc_status overlapped_step(View &v, double dt, cudaStream_t st) {
+  nlse2shoc_t H0 = v.hs[0];
+  cudaStream_t cs = H0->comm_st;
+  for (int s = 1; s <= 4; ++s) {
+    for (size_t i = 0; i < v.hs.size(); ++i) {
+      const int nz = int(v.hs[i]->nz);
+      TRY(stage_range(v.hs[i], v.psis[i], s, dt, 0, 2, st));
+      TRY(stage_range(v.hs[i], v.psis[i], s, dt, nz - 2, nz, st));
+    }
+    // stage s's output is stage s+1's input (s = 4: Psi, the next step's stage 1 input)
+    CUDA_TRY(cudaEventRecord(H0->ev_edge, st));
+    CUDA_TRY(cudaStreamWaitEvent(cs, H0->ev_edge, 0));
+    TRY(exchange(v, s == 4 ? 1 : s + 1, cs));
+    CUDA_TRY(cudaEventRecord(H0->ev_recv, cs));
+    for (size_t i = 0; i < v.hs.size(); ++i) {
+      // a real NCCL exchange runs kernels: leave it a few SMs beside the persistent grid
+      nlse2shoc_t H = v.hs[i];
+      H->reserve_sms = (H->sharded && H->nranks > 1) ? 8 : 0;
+      const nlse2shoc_status r = stage_range(H, v.psis[i], s, dt, 2, int(H->nz) - 2, st);
+      H->reserve_sms = 0;
+      TRY(r);
+    }
+    CUDA_TRY(cudaStreamWaitEvent(st, H0->ev_recv, 0));
+  }
+  return NLSE2SHOC_OK;
+}
+
+// Sharded / loopback calls: the edge-first step (3 launches per slab and stage, the exchange
+// and its two events) is captured once into a CUDA graph, NCCL group included, and replayed
+// nsteps times (option CUDA_GRAPH; calls of one step run eagerly).
 static nlse2shoc_status run_rk4_overlapped(View &v, double dt, int64_t nsteps, cudaStream_t st) {
   nlse2shoc_t H0 = v.hs[0];
   if (!H0->comm_st) {
@@ -709,30 +792,24 @@ static nlse2shoc_status run_rk4_overlapped(View &v, double dt, int64_t nsteps, c
     CUDA_TRY(cudaEventCreateWithFlags(&H0->ev_edge, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&H0->ev_recv, cudaEventDisableTiming));
   }
-  cudaStream_t cs = H0->comm_st;
   TRY(exchange(v, 1, st));  // Psi's halos for the first stage
-  for (int64_t n = 0; n < nsteps; ++n)
-    for (int s = 1; s <= 4; ++s) {
-      for (size_t i = 0; i < v.hs.size(); ++i) {
-        const int nz = int(v.hs[i]->nz);
-        TRY(stage_range(v.hs[i], v.psis[i], s, dt, 0, 2, st));
-        TRY(stage_range(v.hs[i], v.psis[i], s, dt, nz - 2, nz, st));
-      }
-      // stage s's output is stage s+1's input (s = 4: Psi, the next step's stage 1 input)
-      CUDA_TRY(cudaEventRecord(H0->ev_edge, st));
-      CUDA_TRY(cudaStreamWaitEvent(cs, H0->ev_edge, 0));
-      TRY(exchange(v, s == 4 ? 1 : s + 1, cs));
-      CUDA_TRY(cudaEventRecord(H0->ev_recv, cs));
-      for (size_t i = 0; i < v.hs.size(); ++i) {
-        // a real NCCL exchange runs kernels: leave it a few SMs beside the persistent grid
-        nlse2shoc_t H = v.hs[i];
-        H->reserve_sms = (H->sharded && H->nranks > 1) ? 8 : 0;
-        const nlse2shoc_status r = stage_range(H, v.psis[i], s, dt, 2, int(H->nz) - 2, st);
-        H->reserve_sms = 0;
-        TRY(r);
-      }
-      CUDA_TRY(cudaStreamWaitEvent(st, H0->ev_recv, 0));
-    }
+  if (nsteps < 2 || !H0->opt_graph) {
+    for (int64_t n = 0; n < nsteps; ++n) TRY(overlapped_step(v, dt, st));
+    return NLSE2SHOC_OK;
+  }
+  if (!graph_cached(H0, v.psis[0].ptr, dt, 2)) {
+    if (!H0->cap_st) CUDA_TRY(cudaStreamCreateWithFlags(&H0->cap_st, cudaStreamNonBlocking));
+    for (nlse2shoc_t H : v.hs) H->launches = 0;
+    CUDA_TRY(cudaStreamBeginCapture(H0->cap_st, cudaStreamCaptureModeRelaxed));
+    const nlse2shoc_status r = overlapped_step(v, dt, H0->cap_st);
+    TRY(graph_finish(H0, H0->cap_st, r, v.psis[0].ptr, dt, 2));
+    int64_t per_step = 0;
+    for (nlse2shoc_t H : v.hs) per_step += H->launches;
+    H0->g_launches = per_step;
+  }
+  TRY(graph_replay(H0, nsteps, st));
+  for (nlse2shoc_t H : v.hs) H->launches = 0;
+  H0->launches = H0->g_launches * nsteps;
   return NLSE2SHOC_OK;
 }
 
@@ -742,27 +819,17 @@ static nlse2shoc_status run_rk4_overlapped(View &v, double dt, int64_t nsteps, c
 
 static nlse2shoc_status run_rk4_graph(View &v, double dt, int64_t nsteps, cudaStream_t st) {
   nlse2shoc_t H = v.hs[0];
-  if (!H->cap_st) CUDA_TRY(cudaStreamCreateWithFlags(&H->cap_st, cudaStreamNonBlocking));
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t exec = nullptr;
-  CUDA_TRY(cudaStreamBeginCapture(H->cap_st, cudaStreamCaptureModeRelaxed));
-  nlse2shoc_status r = NLSE2SHOC_OK;
-  for (int s = 1; s <= 4 && r == NLSE2SHOC_OK; ++s) r = stage(H, v.psis[0], s, dt, nullptr, H->cap_st);
-  const cudaError_t ec = cudaStreamEndCapture(H->cap_st, &graph);
-  if (r != NLSE2SHOC_OK) {
-    if (graph) cudaGraphDestroy(graph);
-    return r;
+  if (!graph_cached(H, v.psis[0].ptr, dt, 1)) {
+    if (!H->cap_st) CUDA_TRY(cudaStreamCreateWithFlags(&H->cap_st, cudaStreamNonBlocking));
+    H->launches = 0;
+    CUDA_TRY(cudaStreamBeginCapture(H->cap_st, cudaStreamCaptureModeRelaxed));
+    nlse2shoc_status r = NLSE2SHOC_OK;
+    for (int s = 1; s <= 4 && r == NLSE2SHOC_OK; ++s) r = stage(H, v.psis[0], s, dt, nullptr, H->cap_st);
+    TRY(graph_finish(H, H->cap_st, r, v.psis[0].ptr, dt, 1));
+    H->g_launches = H->launches;
   }
-  if (ec != cudaSuccess) return fail(NLSE2SHOC_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ec));
-  const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
-  cudaGraphDestroy(graph);
-  if (ei != cudaSuccess) return fail(NLSE2SHOC_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei));
-  const int64_t per_step = H->launches;
-  cudaError_t el = cudaSuccess;
-  for (int64_t n = 0; n < nsteps && el == cudaSuccess; ++n) el = cudaGraphLaunch(exec, st);
-  cudaGraphExecDestroy(exec);  // deferred by the driver until the launches complete
-  if (el != cudaSuccess) return fail(NLSE2SHOC_ECUDA, std::string("graph launch: ") + cudaGetErrorString(el));
-  H->launches = per_step * nsteps;
+  TRY(graph_replay(H, nsteps, st));
+  H->launches = H->g_launches * nsteps;
   return NLSE2SHOC_OK;
 }
 
@@ -970,6 +1037,10 @@ static nlse2shoc_status create_impl(nlse2shoc_t *out, int dims, const int64_t N[
     else if (cudaMemcpy(H->vtab, host.data(), host.size(), cudaMemcpyHostToDevice) != cudaSuccess)
       chk(fail(NLSE2SHOC_ECUDA, "table upload failed"));
     H->bytes += host.size();
+  }
+  if (st == NLSE2SHOC_OK) {
+    if (dev_malloc(H, &H->sched, 2 * sizeof(unsigned)) != cudaSuccess) chk(fail(NLSE2SHOC_ENOMEM, "counter allocation failed"));
+    else if (cudaMemset(H->sched, 0, 2 * sizeof(unsigned)) != cudaSuccess) chk(fail(NLSE2SHOC_ECUDA, "counter reset failed"));
   }
   if (st == NLSE2SHOC_OK) {
     H->red_blocks = H->num_sms * 4;
@@ -1210,6 +1281,7 @@ nlse2shoc_status nlse2shoc_set_variant(nlse2shoc_t H, int variant) {
   for (nlse2shoc_t S : H->slabs) TRY(nlse2shoc_set_variant(S, variant));
   if ((variant == 1 || variant == 3) && H->slabs.empty()) TRY(ensure_D(H, variant == 3 ? H->dims : 1));
   H->variant = variant;
+  ++H->gen;
   return NLSE2SHOC_OK;
 }
 
@@ -1224,8 +1296,10 @@ nlse2shoc_status nlse2shoc_set_option(nlse2shoc_t H, int option, int64_t value) 
     case NLSE2SHOC_OPT_REVERSE_ORDER: H->opt_reverse = v != 0; break;
     case NLSE2SHOC_OPT_LEAN_STEPS: H->opt_lean = v & 3; break;
     case NLSE2SHOC_OPT_ZCHUNKS: H->opt_zchunks = v; break;
+    case NLSE2SHOC_OPT_TILE_SCHEDULE: H->opt_sched = v >= 2 ? -1 : v; break;
     default: return fail(NLSE2SHOC_EINVAL, "unknown option");
   }
+  ++H->gen;
   for (nlse2shoc_t S : H->slabs) TRY(nlse2shoc_set_option(S, option, value));
   return NLSE2SHOC_OK;
 }
@@ -1238,6 +1312,7 @@ nlse2shoc_status nlse2shoc_set_scheme(nlse2shoc_t H, int scheme) {
     return fail(NLSE2SHOC_EUNSUPPORTED, "the two-kernel variants are 2SHOC forms");
   for (nlse2shoc_t S : H->slabs) TRY(nlse2shoc_set_scheme(S, scheme));
   H->scheme = scheme;
+  ++H->gen;
   return NLSE2SHOC_OK;
 }
 
@@ -1359,6 +1434,8 @@ void nlse2shoc_destroy(nlse2shoc_t H) {
   }
   if (H->vtab) dev_free(H, H->vtab);
   if (H->red) dev_free(H, H->red);
+  if (H->sched) dev_free(H, H->sched);
+  graph_drop(H);
   if (H->ev_edge) cudaEventDestroy(H->ev_edge);
   if (H->ev_recv) cudaEventDestroy(H->ev_recv);
   if (H->comm_st) cudaStreamDestroy(H->comm_st);

@@ -108,6 +108,7 @@ template <typename R> struct StageParams {
   R cA;                  // phase-A coefficient of the stage-pair kernel (stage_pair.cuh)
   int rev;               // traverse the tiles in reverse order (alternate stages: L2 reuse)
   int lean;              // lean plane steps: bit 1 interior tiles, bit 2 3D face tiles (else general)
+  unsigned *sched;       // dynamic tile schedule: {next tile, finished CTAs} (null: static)
   int zb, ze;            // local planes [zb, ze) this launch computes (edge / interior split)
   int bc;                // 0 Dirichlet, 1 Laplacian-zero, 2 MSD (1D line kernels only)
   int vkind;             // 0 none, 1 harmonic tables, 2 array
@@ -131,6 +132,7 @@ template <int DIMS, typename R> struct Layout {
   static constexpr uint32_t SLOT_BYTES = SLOT * sizeof(cplx<R>);
   static constexpr uint32_t PTILE_BYTES = PTILE * sizeof(cplx<R>);
   static constexpr int NTHREADS = (C::NCW + 1) * 32;
+  static constexpr int RI = 4;  // tile-id ring (dynamic tile schedule): producer -> consumer warps
   static_assert(BW <= 256 && (BW * 8) % 16 == 0, "T box");
   static_assert(BWP <= 256 && (BWP * 8) % 16 == 0, "P box");
   static_assert(C::W * EPC % C::NBOX == 0 && C::TX * EPC % C::NBOXP == 0, "box split");
@@ -162,7 +164,7 @@ template <int DIMS, typename R> struct Layout {
   }
   template <int MODE> __host__ __device__ static constexpr size_t smem_bytes() {
     return size_t(rt<MODE>()) * SLOT_BYTES + size_t(rp<MODE>()) * pa_tiles<MODE>() * PTILE_BYTES +
-           size_t(2 * rt<MODE>() + 2 * rp<MODE>()) * 8;
+           size_t(2 * rt<MODE>() + 2 * rp<MODE>() + 2 * RI) * 8 + size_t(RI) * 4;
   }
 };
 
@@ -267,6 +269,9 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
   CT *pring = reinterpret_cast<CT *>(base + size_t(RT) * LY::SLOT_BYTES);
   uint64_t *bars = reinterpret_cast<uint64_t *>(base + size_t(RT) * LY::SLOT_BYTES + size_t(RP) * NPA * LY::PTILE_BYTES);
   uint64_t *fullT = bars, *emptyT = bars + RT, *fullP = bars + 2 * RT, *emptyP = bars + 2 * RT + RP;
+  constexpr int RI = LY::RI;
+  uint64_t *fullI = bars + 2 * RT + 2 * RP, *emptyI = fullI + RI;
+  int *tid_ring = reinterpret_cast<int *>(emptyI + RI);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -277,6 +282,10 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
     for (int i = 0; i < RP; ++i) {
       mbar_init(&fullP[i], 1);
       mbar_init(&emptyP[i], C::NCW);
+    }
+    for (int i = 0; i < RI; ++i) {
+      mbar_init(&fullI[i], 1);
+      mbar_init(&emptyI[i], C::NCW);
     }
     fence_mbar_init();
   }
@@ -302,7 +311,24 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
       const uint64_t pol_keep = policy_evict_last();
       const uint64_t pol_stream = policy_evict_normal();
       uint32_t tcnt = 0, pcnt = 0;
-      for (int t = blockIdx.x; t < P.ntiles; t += G) {
+      // Tile schedule.  Static: CTA b takes tiles b, b + G, ...  Dynamic (P.sched): the next
+      // tile from a global counter, so tiles are taken in order whatever each CTA's speed and
+      // the x / y neighbours of a tile (t +- 1, t +- ncx) are streamed at nearly the same time
+      // (their halo re-reads hit L2); the id is handed to the consumer warps through a ring.
+      uint32_t icnt = 0;
+      for (;;) {
+        int t;
+        if (P.sched) {
+          t = int(atomicAdd(P.sched, 1u));
+          const uint32_t slot = icnt % RI;
+          mbar_wait_backoff(&emptyI[slot], ((icnt / RI) & 1) ^ 1);
+          tid_ring[slot] = t;
+          mbar_arrive(&fullI[slot]);
+        } else {
+          t = int(blockIdx.x + icnt * G);
+        }
+        ++icnt;
+        if (t >= P.ntiles) break;
         const int tt = P.rev ? P.ntiles - 1 - t : t;  // reversed order: read the L2-resident tail first
         const int chunk = tt / ncol, col = tt % ncol;
         const int x0 = (col % P.ncx) * TX, y0 = (col / P.ncx) * TY;
@@ -368,6 +394,15 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
           if (NPA) produceP(k);
         }
       }
+      if (P.sched) {
+        // this CTA has made its last claim; the last CTA to get here resets the counters for
+        // the next launch on the stream
+        __threadfence();
+        if (atomicAdd(P.sched + 1, 1u) == gridDim.x - 1) {
+          atomicExch(P.sched, 0u);
+          atomicExch(P.sched + 1, 0u);
+        }
+      }
     }
     return;
   }
@@ -390,7 +425,18 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
   uint32_t tcnt = 0, pcnt = 0;
   auto inc = [](int v, int m) { return v + 1 == m ? 0 : v + 1; };
 
-  for (int t = blockIdx.x; t < P.ntiles; t += G) {
+  for (uint32_t icnt = 0;; ++icnt) {
+    int t;
+    if (P.sched) {
+      const uint32_t slot = icnt % RI;
+      mbar_wait(&fullI[slot], (icnt / RI) & 1);
+      t = tid_ring[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&emptyI[slot]);
+    } else {
+      t = int(blockIdx.x + icnt * G);
+    }
+    if (t >= P.ntiles) break;
     const int tt = P.rev ? P.ntiles - 1 - t : t;
     const int chunk = tt / ncol, col = tt % ncol;
     const int x0 = (col % P.ncx) * TX, y0 = (col / P.ncx) * TY;

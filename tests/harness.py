@@ -93,3 +93,79 @@ def sl(dims, lo, cnt):
     """numpy slice (z, y, x order) of box [lo, lo+cnt)."""
     s = [slice(lo[d], lo[d] + cnt[d]) for d in range(dims)]
     return tuple(reversed(s))
+
+
+def oracle_crop_rk4(work, dtype, tlo, tcnt, dt, nsteps, segments=10):
+    """The oracle's Psi after nsteps on the target box [tlo, tlo+tcnt), from runs on shrinking
+    dependency-cone crops.  A crop with margin m around the target (true global faces kept
+    where the target is closer than m to them) is exact at depth >= 8 t from its artificial
+    faces after t steps (4 stages x radius 2, reading R8's tangential taps included), so
+    after a segment of c steps it is cut to margin 8 (nsteps - t - c) and continued.  Every
+    value inside the target is the full-grid oracle's, bit for bit (the oracle arithmetic is
+    unchanged; only points that can no longer influence the target are dropped)."""
+    dims = work["grid"]["dims"]
+    seg = max(1, -(-nsteps // segments))
+    lo, cnt = crop_box(work, tlo, tcnt, nsteps)
+    psi = psi0_host(work, dtype, lo, cnt).astype(np.complex128)
+    t = 0
+    while t < nsteps:
+        c = min(seg, nsteps - t)
+        psi = oracle.rk4(oracle_problem(work, lo, cnt), psi, dt, c)
+        t += c
+        nlo, ncnt = crop_box(work, tlo, tcnt, nsteps - t)
+        rel = [nlo[d] - lo[d] for d in range(3)]
+        psi = np.ascontiguousarray(psi[sl(dims, rel, ncnt)])
+        lo, cnt = nlo, ncnt
+    return psi
+
+
+def gpu_field(work, dtype, slab=64, with_kmax=False):
+    """Psi0 of the whole grid on the device, generated slab by slab on the host, so that
+    1536^3 fields never need a whole copy in host memory.  with_kmax: also return the
+    oracle's k_max of the whole grid, folded from the same host slabs (min/max is exact)."""
+    import torch
+
+    g = work["grid"]
+    dims = g["dims"]
+    shape = tuple(reversed(g["n"][:dims]))
+    out = torch.empty(shape, dtype=torch_dtype(dtype), device="cuda")
+    lo_all, hi_all = np.inf, -np.inf
+    nslow = g["n"][dims - 1]
+    for z0 in range(0, nslow, slab):
+        lo = [0, 0, 0]
+        cnt = list(g["n"])
+        lo[dims - 1] = z0
+        cnt[dims - 1] = min(slab, nslow - z0)
+        h = psi0_host(work, dtype, lo, cnt)
+        out[z0:z0 + cnt[dims - 1]].copy_(torch.from_numpy(h.reshape((cnt[dims - 1],) + shape[1:])))
+        if with_kmax:
+            a, b = oracle.N_minmax(oracle.problem_from_work(work, lo=lo, cnt=cnt), h.astype(np.complex128))
+            lo_all, hi_all = min(lo_all, a), max(hi_all, b)
+    if with_kmax:
+        return out, oracle.kmax_from_N(dims, g["h"][:dims], work["a"], lo_all, hi_all)
+    return out
+
+
+def compare(got, want, tol, what=""):
+    """Relative L2 (the north star's measure) and the per-element max norm relative to the
+    box's largest |Psi| (catches errors confined to a few points, e.g. a wrong ghost on one
+    tile edge); both must be <= tol.  Each comparison is appended to $PARITY_LOG (JSON lines)
+    when that is set, so the margins can be reported."""
+    got = np.asarray(got, dtype=np.complex128)
+    want = np.asarray(want, dtype=np.complex128)
+    if not np.any(want):
+        # a region where the oracle is exactly zero (e.g. outside C3's Thomas-Fermi support):
+        # relative measures are undefined, the GPU must be exactly zero too
+        assert not np.any(got), (what, "oracle is zero here, GPU is not")
+        what += " (zero region: exact)"
+    rel = rel_l2(got, want)
+    mx = float(np.abs(got - want).max() / max(np.abs(want).max(), 1e-300))
+    import json
+    import os
+
+    path = os.environ.get("PARITY_LOG")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps({"what": what, "rel_l2": rel, "max_rel": mx, "tol": tol, "points": int(want.size)}) + "\n")
+    assert rel <= tol and mx <= tol, (what, rel, mx, tol)
+    return rel, mx

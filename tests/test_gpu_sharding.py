@@ -86,3 +86,42 @@ def test_nccl_sharded_handle_single_rank():
     assert len(uid) == 128
     got, _ = _run(w, "c64", {"uid": uid, "rank": 0, "nranks": 1}, 0, 4, 1e-4, psi0)
     assert np.array_equal(got.view(np.uint8), ref.view(np.uint8))
+
+
+@pytest.mark.parametrize("nslabs", [2, 3, 8])
+@pytest.mark.parametrize("dims,n,bc,dtype,V", [
+    (3, (37, 19, 48), "dirichlet", "c64", "harmonic"), (3, (40, 33, 41), "lapzero", "c128", "none"),
+    (3, (21, 18, 50), "dirichlet", "c128", "array"), (2, (70, 64), "lapzero", "c64", "harmonic")])
+def test_loopback_matches_oracle(dims, n, bc, dtype, V, nslabs):
+    """The sharded decomposition against the oracle itself (not only against the single
+    slab): seams of every slab, the overlapped edge-first schedule (>= 8 planes per slab for
+    P = 2, 3), 10 steps at 0.8 k_max."""
+    import oracle
+
+    w = configs.SMALL(dims, n, bc, dtype=dtype, V=V, noise=0.05)
+    psi0 = H.psi0_host(w, dtype)
+    P = H.oracle_problem(w)
+    dt = 0.8 * oracle.kmax(P, psi0.astype(np.complex128))
+    got, _ = _run(w, dtype, {"loopback": nslabs}, 0, 10, dt, psi0)
+    ref = oracle.rk4(P, psi0.astype(np.complex128), dt, 10)
+    H.compare(got, ref, H.TOL[dtype], f"loopback P={nslabs} {dims}D {bc} {dtype} {V} 10 steps")
+
+
+def test_loopback_C4_seams_match_oracle():
+    """C4 768^3 split like an 8-GPU run: boxes straddling the seams z = 96, 384 and 672 (at a
+    global corner, in the ring core, at an x-face) after 10 steps against oracle crops."""
+    import paper_1109_1027_b200 as nl
+
+    w = configs.C4()
+    g, kmax = H.gpu_field(w, "c64", with_kmax=True)
+    dt = 0.8 * kmax
+    S8 = nl.solver_from_work(w, "c64", shard={"loopback": 8})
+    S8.rk4(g, dt, 10)
+    T = [([0, 0, 88], [16, 16, 16]), ([376, 370, 376], [16, 20, 16]), ([0, 400, 664], [12, 16, 16])]
+    got = [g[H.sl(3, a, b)].cpu().numpy() for a, b in T]
+    S8.close()
+    del g
+    torch.cuda.empty_cache()
+    for (tlo, tcnt), gb in zip(T, got):
+        want = H.oracle_crop_rk4(w, "c64", tlo, tcnt, dt, 10)
+        H.compare(gb, want, 1e-5, f"C4 loopback P=8 10 steps, seam box {tlo}+{tcnt}")
