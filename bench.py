@@ -249,6 +249,8 @@ def run_ours(args):
     if work["grid"]["dims"] == 1 and ws > 1:
         raise SystemExit("1D configs are replicas only (DESIGN.md §8): run --gpus 1")
     S = nl.solver_from_work(work, dtype, shard=shard)
+    if ws > 1 and args.exchange == "fused":
+        S.connect_peers()  # halo exchange fused into the stage kernels over CUDA IPC / NVLink
     ctype = torch.complex64 if dtype == "c64" else torch.complex128
     g = work["grid"]
     npts_global = int(np.prod(g["n"][:3]))
@@ -334,7 +336,7 @@ def run_ours(args):
             "dtype": "c64 (fp32 pairs)" if dtype == "c64" else "c128 (fp64 pairs)", "data": "synthetic",
             "config": {"workload": WORKLOADS[wl], "grid": g["n"][:dims], "bc": work["bc"],
                        "V": work["V"]["kind"], "dt": dt, "kmax": kmax,
-                       "parallelism": f"z-slab x{ws}" if ws > 1 else "single GPU",
+                       "parallelism": f"z-slab x{ws}, {args.exchange} halo exchange" if ws > 1 else "single GPU",
                        "l2": f"inputs ({host.numel() * host.element_size() / 2**30:.2f} GiB per field per GPU) vs "
                              "L2 126 MB: no flush" + (" (C2: fields comparable to L2, DRAM bytes can fall "
                                                       "below algorithmic)" if wl == "C2" else "")},
@@ -371,6 +373,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", default="C4", choices=["C4", "C5W", "C5S", "C3", "C2"])
     ap.add_argument("--dtype", default=None, choices=["c64", "c128"])
+    ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
+                    help="N>1: halo exchange fused into the stage kernels (peer stores + counters) or NCCL send/recv")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

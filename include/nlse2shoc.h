@@ -106,6 +106,22 @@ nlse2shoc_status nlse2shoc_get_unique_id(void *id128);
 nlse2shoc_status nlse2shoc_create_sharded(nlse2shoc_t *out, int dims, const int64_t N[3], const double h[3],
                                           double a, double s, const nlse2shoc_potential *V, nlse2shoc_bc bc,
                                           nlse2shoc_dtype dtype, const void *id128, int rank, int nranks);
+/* Halo exchange fused into the stage kernels (the
+ * compact stencil keeps the exchange to 2 planes per side).  With peers connected, rk4 runs
+ * each RK4 stage as one kernel launch per rank that also stores its two edge planes on each
+ * side straight into the neighbour's halo buffer (CUDA IPC mapping over NVLink) and raises an
+ * arrival counter there with a system-scope atomic; a kernel reading its halo planes first
+ * waits on its own counter.  No NCCL call and no separate exchange step remain in the step
+ * (one NCCL send/recv of Psi's halos per rk4 call).  Option FUSED_EXCHANGE switches back to
+ * the NCCL exchange.  Loopback handles connect their virtual slabs automatically.
+ *  ipc_handle:    64-byte CUDA IPC handle of this rank's halo arena (cudaMalloc'd at create).
+ *  connect_peers: open the neighbours' handles: lower64 iff rank > 0, upper64 iff
+ *                 rank < nranks-1 (EINVAL otherwise, or if already connected).  Each rank
+ *                 must connect before its next rk4 call; the binding's Solver.connect_peers()
+ *                 gathers the handles with torch.distributed.                              */
+nlse2shoc_status nlse2shoc_ipc_handle(nlse2shoc_t, void *handle64);
+nlse2shoc_status nlse2shoc_connect_peers(nlse2shoc_t, const void *lower64, const void *upper64);
+
 /* Single-GPU emulation of the z-slab sharding (2D/3D): one handle holding nslabs virtual
  * slabs, split exactly like nlse2shoc_split, that exchange their 2-plane halos by
  * device-to-device copies instead of NCCL and run the same kernels as real shards.  The
@@ -184,6 +200,9 @@ nlse2shoc_status nlse2shoc_set_scheme(nlse2shoc_t, int scheme);
  *                    dynamic in 3D (C4 8.83 -> 8.07 ms/step), static in 2D (C3: dynamic
  *                    is 17 % slower).  Dynamic needs the calls on a handle to be ordered
  *                    on one stream at a time (the counter is the handle's).
+ *  FUSED_EXCHANGE [1] sharded / loopback handles with peers: halo exchange fused into the
+ *                    stage kernels (see nlse2shoc_connect_peers); 0 = the edge-first NCCL /
+ *                    copy exchange (OVERLAP).
  * Single-slab and sharded rk4 calls keep their instantiated CUDA graph and replay it in
  * later calls with the same psi pointer and dt (any set_* call drops it).
  * EINVAL for an unknown option or a negative value.                                     */
@@ -194,7 +213,8 @@ typedef enum {
   NLSE2SHOC_OPT_REVERSE_ORDER = 3,
   NLSE2SHOC_OPT_LEAN_STEPS = 4,
   NLSE2SHOC_OPT_ZCHUNKS = 5,
-  NLSE2SHOC_OPT_TILE_SCHEDULE = 6
+  NLSE2SHOC_OPT_TILE_SCHEDULE = 6,
+  NLSE2SHOC_OPT_FUSED_EXCHANGE = 7
 } nlse2shoc_option;
 nlse2shoc_status nlse2shoc_set_option(nlse2shoc_t, int option, int64_t value);
 
@@ -232,7 +252,12 @@ nlse2shoc_status nlse2shoc_set_allocator(nlse2shoc_alloc_fn alloc, nlse2shoc_fre
 
 const char *nlse2shoc_strerror(nlse2shoc_status);
 const char *nlse2shoc_last_error(void);
-/* Library version string, e.g. "nlse2shoc 0.1 sm_100a nccl". */
+/* Checked build (libnlse2shoc_checked.so, -DNLSE_CHECKED): number of global stores of the
+ * 2D/3D stage kernels that fell outside their buffer (skipped, not performed) since load;
+ * syncs the device.  -1 in normal builds (no checks compiled), -2 on a CUDA error.      */
+int64_t nlse2shoc_checked_violations(void);
+
+/* Library version string, e.g. "nlse2shoc 0.2 sm_100a nccl" (" checked" appended). */
 const char *nlse2shoc_version(void);
 void nlse2shoc_destroy(nlse2shoc_t);
 

@@ -15,6 +15,7 @@ __all__ = [
     "Solver", "NLSE2SHOCError", "nlse2shoc_create", "nlse2shoc_create_sharded", "nlse2shoc_get_unique_id",
     "nlse2shoc_laplacian", "nlse2shoc_rk4", "nlse2shoc_stability_bound", "nlse2shoc_check_finite",
     "nlse2shoc_split", "nlse2shoc_version", "solver_from_work", "nlse2shoc_create_loopback", "nlse2shoc_set_option",
+    "nlse2shoc_ipc_handle", "nlse2shoc_connect_peers", "peer_handles", "gather_peer_handles",
 ]
 
 
@@ -120,11 +121,41 @@ def nlse2shoc_check_finite(H, psi, stream=None):
 
 
 OPTIONS = {"cuda_graph": 0, "overlap": 1, "resident_1d": 2, "reverse_order": 3, "lean_steps": 4, "zchunks": 5,
-           "tile_schedule": 6}
+           "tile_schedule": 6, "fused_exchange": 7}
 
 
 def nlse2shoc_set_option(H, option, value: int):
     check(lib().nlse2shoc_set_option(H, OPTIONS.get(option, option), int(value)), "set_option")
+
+
+def nlse2shoc_ipc_handle(H) -> bytes:
+    buf = (ctypes.c_ubyte * 64)()
+    check(lib().nlse2shoc_ipc_handle(H, buf), "ipc_handle")
+    return bytes(buf)
+
+
+def nlse2shoc_connect_peers(H, lower: bytes | None, upper: bytes | None):
+    lo = (ctypes.c_ubyte * 64).from_buffer_copy(lower) if lower is not None else None
+    hi = (ctypes.c_ubyte * 64).from_buffer_copy(upper) if upper is not None else None
+    check(lib().nlse2shoc_connect_peers(H, lo, hi), "connect_peers")
+
+
+def peer_handles(handles, rank: int, nranks: int):
+    """The (lower, upper) neighbours' entries of an all-gathered list (None at the ends)."""
+    if len(handles) != nranks:
+        raise ValueError(f"expected {nranks} handles, got {len(handles)}")
+    return (handles[rank - 1] if rank > 0 else None), (handles[rank + 1] if rank < nranks - 1 else None)
+
+
+def gather_peer_handles(mine: bytes, group=None):
+    """All-gather every rank's 64-byte IPC handle over torch.distributed (any backend) and
+    return this rank's (lower, upper) neighbours' handles."""
+    import torch.distributed as dist
+
+    ws, rank = dist.get_world_size(group), dist.get_rank(group)
+    out = [None] * ws
+    dist.all_gather_object(out, mine, group=group)
+    return peer_handles(out, rank, ws)
 
 
 def _check_V_array(V, dims, N, dtype, shard):
@@ -189,6 +220,12 @@ class Solver:
         """Execution-path option (include/nlse2shoc.h nlse2shoc_option): 'cuda_graph',
         'overlap', 'resident_1d', 'reverse_order', 'lean_steps', 'zchunks', 'tile_schedule'."""
         nlse2shoc_set_option(self._h, option, value)
+
+    def connect_peers(self, group=None):
+        """Sharded (NCCL) handles: exchange halo-arena IPC handles with the neighbour ranks
+        (torch.distributed all-gather) and switch rk4 to the fused exchange.  Collective."""
+        lo, hi = gather_peer_handles(nlse2shoc_ipc_handle(self._h), group)
+        nlse2shoc_connect_peers(self._h, lo, hi)
 
     def set_scheme(self, scheme):
         """0/"2shoc" (default) or 1/"cd" (the paper's RK4+CD comparison scheme)."""

@@ -13,6 +13,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libnlse2shoc.so")
+SO_CHECKED = os.path.join(HERE, "libnlse2shoc_checked.so")  # -DNLSE_CHECKED: range-checked stores
 SRC = os.path.join(HERE, "csrc", "nlse2shoc.cu")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -64,6 +64,8 @@ def lib():
             "nlse2shoc_set_variant": [H, ctypes.c_int],
             "nlse2shoc_set_scheme": [H, ctypes.c_int],
             "nlse2shoc_set_option": [H, ctypes.c_int, ctypes.c_int64],
+            "nlse2shoc_ipc_handle": [H, ctypes.c_void_p],
+            "nlse2shoc_connect_peers": [H, ctypes.c_void_p, ctypes.c_void_p],
             "nlse2shoc_laplacian": [H, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p],
             "nlse2shoc_rk4": [H, ctypes.c_void_p, ctypes.c_double, ctypes.c_int64, ctypes.c_void_p],
             "nlse2shoc_stability_bound": [H, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_void_p],
@@ -85,6 +87,9 @@ def lib():
         L.nlse2shoc_last_error.restype = ctypes.c_char_p
         L.nlse2shoc_version.argtypes = []
         L.nlse2shoc_version.restype = ctypes.c_char_p
+        if hasattr(L, "nlse2shoc_checked_violations"):
+            L.nlse2shoc_checked_violations.argtypes = []
+            L.nlse2shoc_checked_violations.restype = ctypes.c_int64
         L.nlse2shoc_destroy.argtypes = [H]
         L.nlse2shoc_destroy.restype = None
         has_alloc = hasattr(L, "nlse2shoc_set_allocator")
@@ -148,8 +153,9 @@ EXPORTS = [
     "nlse2shoc_create", "nlse2shoc_get_unique_id", "nlse2shoc_create_sharded", "nlse2shoc_create_loopback",
     "nlse2shoc_local_extent",
     "nlse2shoc_split", "nlse2shoc_workspace_bytes", "nlse2shoc_set_variant", "nlse2shoc_set_scheme", "nlse2shoc_set_option",
+    "nlse2shoc_ipc_handle", "nlse2shoc_connect_peers",
     "nlse2shoc_laplacian",
     "nlse2shoc_rk4", "nlse2shoc_stability_bound", "nlse2shoc_check_finite", "nlse2shoc_last_launch_count",
     "nlse2shoc_strerror", "nlse2shoc_last_error", "nlse2shoc_version", "nlse2shoc_destroy",
-    "nlse2shoc_set_allocator",
+    "nlse2shoc_set_allocator", "nlse2shoc_checked_violations",
 ]

@@ -172,6 +172,35 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
 __device__ __forceinline__ void st_stream(float4 *p, float4 v) { *p = v; }
 __device__ __forceinline__ void st_stream(double2 *p, double2 v) { *p = v; }
 
+// Checked build (-DNLSE_CHECKED, libnlse2shoc_checked.so; compute-sanitizer is not available
+// on the GPU pool): every global store of the 2D/3D stage kernel is range-checked against
+// the buffer it belongs to; a store outside is skipped and counted, and
+// nlse2shoc_checked_violations() reads the count.  Normal builds compile the checks away.
+#ifdef NLSE_CHECKED
+__device__ unsigned long long g_nlse_violations;
+// n elements of T at p lie inside [base, base + bytes)
+template <typename T> __device__ __forceinline__ bool in_range(const T *p, int n, const void *base, int64_t bytes) {
+  const char *b = reinterpret_cast<const char *>(base), *q = reinterpret_cast<const char *>(p);
+  return base != nullptr && q >= b && q + int64_t(n) * int64_t(sizeof(T)) <= b + bytes;
+}
+#define NLSE_STORE_OK(p, n, base, bytes) (in_range((p), (n), (base), (bytes)) ? true : (atomicAdd(&g_nlse_violations, 1ull), false))
+#else
+#define NLSE_STORE_OK(p, n, base, bytes) true
+#endif
+
+// Fused halo exchange (stage_stream.cuh): wait until a counter that a neighbour slab raises
+// with system-scope atomics reaches target, then order the halo reads that follow through the
+// async proxy (TMA) after the acquire.
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void wait_counter(const unsigned long long *p, unsigned long long target) {
+  while (ld_acquire_sys(p) < target) __nanosleep(128);
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

@@ -121,6 +121,20 @@ struct nlse2shoc_s {
   int g_kind = 0;
   uint64_t gen = 0, g_gen = 0;
   int64_t g_launches = 0;
+  // z-slab halos: one cudaMalloc arena (exportable by CUDA IPC) holding, per field role
+  // (0 Psi, 1 T_A, 2 T_B, 3 acc), the 2 low and 2 high halo planes, then two arrival counters
+  // of the fused exchange: cnt[0] raised by the lower neighbour, cnt[1] by the upper one
+  char *arena = nullptr;
+  size_t halo_bytes = 0, arena_bytes = 0;
+  unsigned long long *cnt = nullptr;
+  // fused exchange: the neighbours' halo buffers per role and counters
+  void *peer_lo[4] = {}, *peer_hi[4] = {};
+  unsigned long long *peer_sig_lo = nullptr, *peer_sig_hi = nullptr;
+  void *ipc_lo = nullptr, *ipc_hi = nullptr;  // neighbours' arenas opened by CUDA IPC
+  bool peers = false;                          // peer pointers connected
+  bool fusing = false;                         // the running rk4 call mirrors edge planes
+  int opt_fused = 1;                           // option FUSED_EXCHANGE
+  unsigned long long fused_epoch = 0;          // mirrored stage launches so far
   // loopback (single-GPU emulation of z-slab sharding, SURVEY §4 T3'): virtual slabs that
   // exchange halos by device copies instead of NCCL; empty for ordinary handles
   std::vector<nlse2shoc_s *> slabs;
@@ -518,6 +532,13 @@ static nlse2shoc_status launch_two(int, int stage, const cplx<R> *in, const cplx
 // Write-light combine: the default of 2D/3D handles (variant 0) and variant 5.
 static bool write_light(const nlse2shoc_t H) { return H->variant == 0 || H->variant == 5; }
 
+// role of stage s's stencil input in the halo arena: 0 Psi, 1 T_A, 2 T_B, 3 acc
+static int input_role(const nlse2shoc_t H, int s) {
+  if (s == 1 || s == 5) return 0;
+  if (s == 4 && write_light(H)) return 3;
+  return s == 3 ? 2 : 1;
+}
+
 // (write-light: stage 3 writes T_C into acc's buffer, which is stage 4's stencil input)
 static Field &stage_input(nlse2shoc_t H, Field &psi, int s) {
   if (s == 4 && write_light(H)) return H->acc;
@@ -560,6 +581,19 @@ static nlse2shoc_status launch_stage(nlse2shoc_t H, Field &psi, int s, double dt
   P.in_P[1] = reinterpret_cast<const cplx<R> *>(H->acc.ptr);
   P.in_P[2] = nullptr;
   Field &in = stage_input(H, psi, s);
+  if (H->fusing && s <= 4) {
+    // fused exchange: this stage's output is the next stage's input (stage 4: Psi^{n+1})
+    const int r = input_role(H, s == 4 ? 1 : s + 1);
+    P.mir_lo = reinterpret_cast<cplx<R> *>(H->peer_lo[r]);
+    P.mir_hi = reinterpret_cast<cplx<R> *>(H->peer_hi[r]);
+    P.sig_lo = H->peer_sig_lo;
+    P.sig_hi = H->peer_sig_hi;
+    P.cnt = H->cnt;
+    P.wait_lo = H->peer_lo[r] != nullptr;
+    P.wait_hi = H->peer_hi[r] != nullptr;
+    P.peer_sys = H->ipc_lo != nullptr || H->ipc_hi != nullptr;
+    P.rev = 0;  // edge chunks first (the kernel's chunk order), not the reversed traversal
+  }
   cplx<R> *pPsi = reinterpret_cast<cplx<R> *>(psi.ptr), *pA = reinterpret_cast<cplx<R> *>(H->TA.ptr),
           *pB = reinterpret_cast<cplx<R> *>(H->TB.ptr), *pAcc = reinterpret_cast<cplx<R> *>(H->acc.ptr);
   // reconstructed-accumulator form (13 transfers per point-step): variant 6
@@ -833,6 +867,52 @@ static nlse2shoc_status run_rk4_graph(View &v, double dt, int64_t nsteps, cudaSt
   return NLSE2SHOC_OK;
 }
 
+// Fused exchange: every slab runs each stage as ONE launch whose kernel
+// stores its edge planes into the neighbours' halo buffers and raises their arrival counters;
+// there is no exchange step and no edge / interior split.  Fused variants, 2D/3D, slabs with
+// connected peers (loopback siblings, or ranks joined by nlse2shoc_connect_peers).
+static bool fused_ok(const View &v) {
+  for (nlse2shoc_t H : v.hs)
+    if (!H->peers || !H->opt_fused || H->dims < 2 ||
+        (H->variant != 0 && H->variant != 2 && H->variant != 5 && H->variant != 6))
+      return false;
+  return true;
+}
+
+static nlse2shoc_status fused_step(View &v, double dt, cudaStream_t st) {
+  for (int s = 1; s <= 4; ++s)
+    for (size_t i = 0; i < v.hs.size(); ++i) {
+      v.hs[i]->fusing = true;
+      const nlse2shoc_status r = stage(v.hs[i], v.psis[i], s, dt, nullptr, st);
+      v.hs[i]->fusing = false;
+      TRY(r);
+    }
+  return NLSE2SHOC_OK;
+}
+
+static nlse2shoc_status run_rk4_fused(View &v, double dt, int64_t nsteps, cudaStream_t st) {
+  nlse2shoc_t H0 = v.hs[0];
+  TRY(exchange(v, 1, st));  // the caller's Psi: halos of the first stage (once per call)
+  if (nsteps < 2 || !H0->opt_graph) {
+    for (int64_t n = 0; n < nsteps; ++n) TRY(fused_step(v, dt, st));
+    return NLSE2SHOC_OK;
+  }
+  if (!graph_cached(H0, v.psis[0].ptr, dt, 3)) {
+    if (!H0->cap_st) CUDA_TRY(cudaStreamCreateWithFlags(&H0->cap_st, cudaStreamNonBlocking));
+    for (nlse2shoc_t H : v.hs) H->launches = 0;
+    CUDA_TRY(cudaStreamBeginCapture(H0->cap_st, cudaStreamCaptureModeRelaxed));
+    const nlse2shoc_status r = fused_step(v, dt, H0->cap_st);
+    TRY(graph_finish(H0, H0->cap_st, r, v.psis[0].ptr, dt, 3));
+    int64_t per_step = 0;
+    for (nlse2shoc_t H : v.hs) per_step += H->launches;
+    H0->g_launches = per_step;
+  }
+  TRY(graph_replay(H0, nsteps, st));
+  for (nlse2shoc_t H : v.hs) H->launches = 0;
+  H0->launches = H0->g_launches * nsteps;
+  return NLSE2SHOC_OK;
+}
+
 static nlse2shoc_status run_rk4(View &v, double dt, int64_t nsteps, cudaStream_t st) {
   if (v.hs.size() == 1 && v.hs[0]->variant == 4) return rk4_pairs(v.hs[0], v.psis[0], dt, nsteps, st);
   if (v.hs.size() == 1 && resident_ok(v.hs[0])) {
@@ -840,6 +920,7 @@ static nlse2shoc_status run_rk4(View &v, double dt, int64_t nsteps, cudaStream_t
     return H->dtype == NLSE2SHOC_C64 ? rk4_resident_1d<float>(H, v.psis[0], dt, nsteps, st)
                                      : rk4_resident_1d<double>(H, v.psis[0], dt, nsteps, st);
   }
+  if (fused_ok(v)) return run_rk4_fused(v, dt, nsteps, st);
   if (overlap_ok(v)) return run_rk4_overlapped(v, dt, nsteps, st);
   if (v.hs.size() == 1 && !v.hs[0]->sharded && nsteps >= 4 && v.hs[0]->opt_graph) return run_rk4_graph(v, dt, nsteps, st);
   for (int64_t n = 0; n < nsteps; ++n)
@@ -851,18 +932,27 @@ static nlse2shoc_status run_rk4(View &v, double dt, int64_t nsteps, cudaStream_t
 }
 
 // ------------------------------------------------------------------------------ create
-static nlse2shoc_status alloc_field(nlse2shoc_t H, Field &f, bool halos) {
+static nlse2shoc_status alloc_field(nlse2shoc_t H, Field &f) {
   const size_t bytes = size_t(H->local_elems) * H->S;
   CUDA_TRY(dev_malloc(H, &f.ptr, bytes));
   H->bytes += bytes;
-  if (halos && H->sharded) {
-    const size_t hb = size_t(2 * H->plane) * H->S;
-    CUDA_TRY(dev_malloc(H, &f.halo_lo, hb));
-    CUDA_TRY(dev_malloc(H, &f.halo_hi, hb));
-    CUDA_TRY(cudaMemsetAsync(f.halo_lo, 0, hb));
-    CUDA_TRY(cudaMemsetAsync(f.halo_hi, 0, hb));
-    H->bytes += 2 * hb;
+  return NLSE2SHOC_OK;
+}
+
+// Halo arena of a sharded handle (layout in nlse2shoc_s).  cudaMalloc, not the caller's
+// allocator: its base is what CUDA IPC exports to the neighbour ranks.
+static Field &role_field(nlse2shoc_t H, int r) { return r == 0 ? H->psiw : (r == 1 ? H->TA : (r == 2 ? H->TB : H->acc)); }
+static nlse2shoc_status alloc_arena(nlse2shoc_t H) {
+  H->halo_bytes = ((size_t(2 * H->plane) * H->S + 255) / 256) * 256;
+  H->arena_bytes = 8 * H->halo_bytes + 256;
+  CUDA_TRY(cudaMalloc(reinterpret_cast<void **>(&H->arena), H->arena_bytes));
+  CUDA_TRY(cudaMemset(H->arena, 0, H->arena_bytes));
+  H->bytes += H->arena_bytes;
+  for (int r = 0; r < 4; ++r) {
+    role_field(H, r).halo_lo = H->arena + size_t(2 * r) * H->halo_bytes;
+    role_field(H, r).halo_hi = H->arena + size_t(2 * r + 1) * H->halo_bytes;
   }
+  H->cnt = reinterpret_cast<unsigned long long *>(H->arena + 8 * H->halo_bytes);
   return NLSE2SHOC_OK;
 }
 
@@ -995,8 +1085,20 @@ static nlse2shoc_status create_impl(nlse2shoc_t *out, int dims, const int64_t N[
       chk(create_impl(&S, dims, N, h, a, s, V, bc, dtype, i, P, nullptr, 1));
       if (S) H->slabs.push_back(S);
     }
+    // virtual slabs are each other's peers (same device): the fused exchange needs no IPC
+    for (size_t i = 0; st == NLSE2SHOC_OK && i < H->slabs.size(); ++i) {
+      nlse2shoc_t S = H->slabs[i];
+      nlse2shoc_t lo = i > 0 ? H->slabs[i - 1] : nullptr, hi = i + 1 < H->slabs.size() ? H->slabs[i + 1] : nullptr;
+      for (int r = 0; r < 4; ++r) {
+        S->peer_lo[r] = lo ? role_field(lo, r).halo_hi : nullptr;
+        S->peer_hi[r] = hi ? role_field(hi, r).halo_lo : nullptr;
+      }
+      S->peer_sig_lo = lo ? lo->cnt + 1 : nullptr;  // the lower slab's "from above" counter
+      S->peer_sig_hi = hi ? hi->cnt : nullptr;      // the upper slab's "from below" counter
+      S->peers = true;
+    }
     if (st == NLSE2SHOC_OK && H->pitch != H->nx) {
-      chk(alloc_field(H, H->psiw, false));
+      chk(alloc_field(H, H->psiw));
       if (st == NLSE2SHOC_OK && dev_malloc(H, &H->Lw, size_t(H->local_elems) * H->S) != cudaSuccess)
         chk(fail(NLSE2SHOC_ENOMEM, "staging allocation failed"));
     }
@@ -1008,21 +1110,15 @@ static nlse2shoc_status create_impl(nlse2shoc_t *out, int dims, const int64_t N[
     }
     return st;
   }
-  chk(alloc_field(H, H->TA, true));
-  chk(alloc_field(H, H->TB, true));
-  chk(alloc_field(H, H->acc, true));  // halos: stage 4's stencil input in variant 5
+  chk(alloc_field(H, H->TA));
+  chk(alloc_field(H, H->TB));
+  chk(alloc_field(H, H->acc));
   if (st == NLSE2SHOC_OK && H->pitch != H->nx && !H->loop_member) {
-    chk(alloc_field(H, H->psiw, true));
+    chk(alloc_field(H, H->psiw));
     if (st == NLSE2SHOC_OK && dev_malloc(H, &H->Lw, size_t(H->local_elems) * H->S) != cudaSuccess)
       chk(fail(NLSE2SHOC_ENOMEM, "staging allocation failed"));
   }
-  if (st == NLSE2SHOC_OK && H->sharded && (H->pitch == H->nx || H->loop_member)) {
-    // halo buffers for the caller's Psi (zero-copy path)
-    const size_t hb = size_t(2 * H->plane) * H->S;
-    if (dev_malloc(H, &H->psiw.halo_lo, hb) != cudaSuccess || dev_malloc(H, &H->psiw.halo_hi, hb) != cudaSuccess)
-      chk(fail(NLSE2SHOC_ENOMEM, "halo allocation failed"));
-    H->bytes += 2 * hb;
-  }
+  if (st == NLSE2SHOC_OK && H->sharded) chk(alloc_arena(H));  // halos of all four field roles
   if (st == NLSE2SHOC_OK) {
     chk(encode_maps(H, H->TA));
     chk(encode_maps(H, H->TB));
@@ -1297,10 +1393,53 @@ nlse2shoc_status nlse2shoc_set_option(nlse2shoc_t H, int option, int64_t value) 
     case NLSE2SHOC_OPT_LEAN_STEPS: H->opt_lean = v & 3; break;
     case NLSE2SHOC_OPT_ZCHUNKS: H->opt_zchunks = v; break;
     case NLSE2SHOC_OPT_TILE_SCHEDULE: H->opt_sched = v >= 2 ? -1 : v; break;
+    case NLSE2SHOC_OPT_FUSED_EXCHANGE: H->opt_fused = v != 0; break;
     default: return fail(NLSE2SHOC_EINVAL, "unknown option");
   }
   ++H->gen;
   for (nlse2shoc_t S : H->slabs) TRY(nlse2shoc_set_option(S, option, value));
+  return NLSE2SHOC_OK;
+}
+
+nlse2shoc_status nlse2shoc_ipc_handle(nlse2shoc_t H, void *handle64) {
+  if (!H || !handle64) return fail(NLSE2SHOC_EINVAL, "NULL argument");
+  if (!H->arena || H->slabs.size() || H->loop_member) return fail(NLSE2SHOC_EINVAL, "not a sharded (NCCL) handle");
+  DeviceGuard dg(H->device);
+  cudaIpcMemHandle_t h;
+  static_assert(sizeof(h) == 64, "CUDA IPC handle size");
+  CUDA_TRY(cudaIpcGetMemHandle(&h, H->arena));
+  std::memcpy(handle64, &h, sizeof(h));
+  return NLSE2SHOC_OK;
+}
+
+nlse2shoc_status nlse2shoc_connect_peers(nlse2shoc_t H, const void *lower64, const void *upper64) {
+  if (!H) return fail(NLSE2SHOC_EINVAL, "NULL handle");
+  if (!H->arena || H->slabs.size() || H->loop_member) return fail(NLSE2SHOC_EINVAL, "not a sharded (NCCL) handle");
+  if ((lower64 != nullptr) != (H->rank > 0) || (upper64 != nullptr) != (H->rank < H->nranks - 1))
+    return fail(NLSE2SHOC_EINVAL, "give exactly the neighbours this rank has (lower iff rank > 0, upper iff rank < nranks-1)");
+  if (H->peers) return fail(NLSE2SHOC_EINVAL, "peers already connected");
+  DeviceGuard dg(H->device);
+  char *base[2] = {nullptr, nullptr};
+  const void *hs[2] = {lower64, upper64};
+  for (int i = 0; i < 2; ++i) {
+    if (!hs[i]) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, hs[i], sizeof(h));
+    void *p = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    base[i] = reinterpret_cast<char *>(p);
+    (i ? H->ipc_hi : H->ipc_lo) = p;
+  }
+  // every rank's arena has the same layout (same plane size): role r's low halo at 2r, high at
+  // 2r+1 halo blocks, counters after the 8 blocks
+  for (int r = 0; r < 4; ++r) {
+    H->peer_lo[r] = base[0] ? base[0] + size_t(2 * r + 1) * H->halo_bytes : nullptr;
+    H->peer_hi[r] = base[1] ? base[1] + size_t(2 * r) * H->halo_bytes : nullptr;
+  }
+  H->peer_sig_lo = base[0] ? reinterpret_cast<unsigned long long *>(base[0] + 8 * H->halo_bytes) + 1 : nullptr;
+  H->peer_sig_hi = base[1] ? reinterpret_cast<unsigned long long *>(base[1] + 8 * H->halo_bytes) : nullptr;
+  H->peers = true;
+  ++H->gen;
   return NLSE2SHOC_OK;
 }
 
@@ -1413,11 +1552,27 @@ const char *nlse2shoc_strerror(nlse2shoc_status st) {
 
 const char *nlse2shoc_last_error(void) { return g_last_error.c_str(); }
 
-const char *nlse2shoc_version(void) {
-#ifdef NLSE_WITH_NCCL
-  return "nlse2shoc 0.1 sm_100a nccl";
+int64_t nlse2shoc_checked_violations(void) {
+#ifdef NLSE_CHECKED
+  unsigned long long v = 0;
+  if (cudaDeviceSynchronize() != cudaSuccess || cudaMemcpyFromSymbol(&v, g_nlse_violations, sizeof(v)) != cudaSuccess)
+    return -2;
+  return int64_t(v);
 #else
-  return "nlse2shoc 0.1 sm_100a";
+  return -1;
+#endif
+}
+
+const char *nlse2shoc_version(void) {
+#ifdef NLSE_CHECKED
+#define NLSE_VARIANT_TAG " checked"
+#else
+#define NLSE_VARIANT_TAG ""
+#endif
+#ifdef NLSE_WITH_NCCL
+  return "nlse2shoc 0.2 sm_100a nccl" NLSE_VARIANT_TAG;
+#else
+  return "nlse2shoc 0.2 sm_100a" NLSE_VARIANT_TAG;
 #endif
 }
 
@@ -1427,11 +1582,11 @@ void nlse2shoc_destroy(nlse2shoc_t H) {
   cudaDeviceSynchronize();
   for (nlse2shoc_t S : H->slabs) nlse2shoc_destroy(S);
   if (H->Lw) dev_free(H, H->Lw);
-  for (Field *f : {&H->TA, &H->TB, &H->acc, &H->psiw, &H->D}) {
+  for (Field *f : {&H->TA, &H->TB, &H->acc, &H->psiw, &H->D})
     if (f->ptr) dev_free(H, f->ptr);
-    if (f->halo_lo) dev_free(H, f->halo_lo);
-    if (f->halo_hi) dev_free(H, f->halo_hi);
-  }
+  if (H->ipc_lo) cudaIpcCloseMemHandle(H->ipc_lo);
+  if (H->ipc_hi) cudaIpcCloseMemHandle(H->ipc_hi);
+  if (H->arena) cudaFree(H->arena);
   if (H->vtab) dev_free(H, H->vtab);
   if (H->red) dev_free(H, H->red);
   if (H->sched) dev_free(H, H->sched);

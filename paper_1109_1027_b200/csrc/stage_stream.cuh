@@ -109,6 +109,19 @@ template <typename R> struct StageParams {
   int rev;               // traverse the tiles in reverse order (alternate stages: L2 reuse)
   int lean;              // lean plane steps: bit 1 interior tiles, bit 2 3D face tiles (else general)
   unsigned *sched;       // dynamic tile schedule: {next tile, finished CTAs} (null: static)
+  // Halo exchange fused into the stage: the output planes 0, 1 (nz-2, nz-1)
+  // are also stored into the lower (upper) neighbour slab's halo buffer of the next stage's
+  // input (mir_lo / mir_hi, peer memory), and each finished edge plane-tile adds 1 to the
+  // neighbour's arrival counter (sig_lo / sig_hi).  Before a tile reads its own halo planes
+  // the producer waits until the counter that neighbour raises (cnt[0] lower, cnt[1] upper)
+  // reaches 2 ncol e, e = this slab's fused-launch epoch (cnt[2]; kept on the device, so a
+  // captured graph stays valid, and advanced by the CTA that finishes last, cnt[3] counting).
+  // cnt: this slab's {from below, from above, epoch, finished CTAs}.  All null: no fused exchange.
+  cplx<R> *mir_lo, *mir_hi;
+  unsigned long long *sig_lo, *sig_hi;
+  unsigned long long *cnt;
+  int wait_lo, wait_hi;  // this slab has a lower / upper neighbour to wait for
+  int peer_sys;          // neighbours on other GPUs (system-scope fence) or this one (device scope)
   int zb, ze;            // local planes [zb, ze) this launch computes (edge / interior split)
   int bc;                // 0 Dirichlet, 1 Laplacian-zero, 2 MSD (1D line kernels only)
   int vkind;             // 0 none, 1 harmonic tables, 2 array
@@ -294,6 +307,8 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
   const int G = gridDim.x;
   const int chunk_len = (P.ze - P.zb + P.nchunk - 1) / P.nchunk;
   const int ncol = P.ncx * P.ncy;
+  // fused exchange: the two edge chunks (the planes the neighbours wait for) go first
+  auto chunk_of = [&](int i) { return (!P.cnt || P.nchunk < 3) ? i : (i == 0 ? 0 : (i == 1 ? P.nchunk - 1 : i - 1)); };
 
   if (warp == C::NCW) {
     // ------------------------------------------------------------------ producer warp
@@ -311,6 +326,10 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
       const uint64_t pol_keep = policy_evict_last();
       const uint64_t pol_stream = policy_evict_normal();
       uint32_t tcnt = 0, pcnt = 0;
+      // fused exchange: the neighbours' edge planes of the previous stage = 2 ncol plane-tiles
+      // per fused launch, so this launch (epoch e) waits for 2 ncol e arrivals
+      const unsigned long long arrivals =
+          P.cnt ? 2ull * unsigned(ncol) * *reinterpret_cast<volatile unsigned long long *>(P.cnt + 2) : 0ull;
       // Tile schedule.  Static: CTA b takes tiles b, b + G, ...  Dynamic (P.sched): the next
       // tile from a global counter, so tiles are taken in order whatever each CTA's speed and
       // the x / y neighbours of a tile (t +- 1, t +- ncx) are streamed at nearly the same time
@@ -330,17 +349,31 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
         ++icnt;
         if (t >= P.ntiles) break;
         const int tt = P.rev ? P.ntiles - 1 - t : t;  // reversed order: read the L2-resident tail first
-        const int chunk = tt / ncol, col = tt % ncol;
+        const int chunk = chunk_of(tt / ncol), col = tt % ncol;
         const int x0 = (col % P.ncx) * TX, y0 = (col / P.ncx) * TY;
         const int kb = P.zb + chunk * chunk_len, ke = min(P.ze, kb + chunk_len);
+        bool need_lo = P.cnt && P.wait_lo, need_hi = P.cnt && P.wait_hi;
         auto produceT = [&](int p) {
           const uint32_t slot = tcnt % RT, par = (tcnt / RT) & 1;
           mbar_wait_backoff(&emptyT[slot], par ^ 1);
           const CUtensorMap *m = nullptr;
           int pz = p;
           if (p >= 0 && p < P.nz) m = &tm_T;
-          else if (p < 0 && P.has_lo_halo) { m = &tm_lo; pz = p + 2; }
-          else if (p >= P.nz && P.has_hi_halo) { m = &tm_hi; pz = p - P.nz; }
+          else if (p < 0 && P.has_lo_halo) {
+            m = &tm_lo;
+            pz = p + 2;
+            if (need_lo) {  // fused exchange: the lower neighbour's edge planes have landed
+              wait_counter(P.cnt, arrivals);
+              need_lo = false;
+            }
+          } else if (p >= P.nz && P.has_hi_halo) {
+            m = &tm_hi;
+            pz = p - P.nz;
+            if (need_hi) {
+              wait_counter(P.cnt + 1, arrivals);
+              need_hi = false;
+            }
+          }
           if (m) {
             mbar_arrive_expect_tx(&fullT[slot], LY::SLOT_BYTES);
             CT *dst = ring + size_t(slot) * LY::SLOT;
@@ -438,7 +471,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
     }
     if (t >= P.ntiles) break;
     const int tt = P.rev ? P.ntiles - 1 - t : t;
-    const int chunk = tt / ncol, col = tt % ncol;
+    const int chunk = chunk_of(tt / ncol), col = tt % ncol;
     const int x0 = (col % P.ncx) * TX, y0 = (col / P.ncx) * TY;
     const int kb = P.zb + chunk * chunk_len, ke = min(P.ze, kb + chunk_len);
     const uint32_t tbase = tcnt;  // ring counter of plane kb-2
@@ -480,7 +513,8 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
     uint32_t ph2 = ((tbase + 4) / RT) & 1;
     int sp = int(pcnt % RPM);
     uint32_t php = (pcnt / RPM) & 1;
-    cplx<R> *outT = P.out_T + int64_t(kb) * P.plane + int64_t(y0 + ly0) * P.pitch + (x0 + lx0);
+    const int64_t ooff = int64_t(y0 + ly0) * P.pitch + (x0 + lx0);  // this thread's in-plane offset
+    cplx<R> *outT = P.out_T + int64_t(kb) * P.plane + ooff;
     cplx<R> *outA = (LY::template writes_acc<MODE>()) ? P.out_acc + (outT - P.out_T) : nullptr;
 
     // streamed-axis potential table, software-pipelined one plane ahead (its global load
@@ -491,6 +525,26 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
       const R v = vz_pre;
       if (has_vz && k + 1 < ke) vz_pre = P.vz[z0 + k + 1];
       return v;
+    };
+    // fused exchange: output plane k also goes to a neighbour's halo (null: it does not)
+    auto mirror_lo = [&](int k) -> CT * { return (P.mir_lo && k < 2) ? P.mir_lo + int64_t(k) * P.plane + ooff : nullptr; };
+    auto mirror_hi = [&](int k) -> CT * {
+      return (P.mir_hi && k >= nz - 2) ? P.mir_hi + int64_t(k - (nz - 2)) * P.plane + ooff : nullptr;
+    };
+    // after a mirrored plane: the consumer warps meet, then one thread makes their stores
+    // visible to the neighbour and counts the plane-tile there
+    // (bar.sync orders the other consumer threads' stores before thread 0's fence, which is
+    // cumulative; system scope for peers on other GPUs, device scope for loopback slabs)
+    auto signal = [&](int k) {
+      const bool lo = P.mir_lo && k < 2, hi = P.mir_hi && k >= nz - 2;
+      if (!lo && !hi) return;
+      named_bar_sync(1, C::NCW * 32);
+      if (threadIdx.x == 0) {
+        if (P.peer_sys) __threadfence_system();
+        else __threadfence();
+        if (lo) atomicAdd_system(P.sig_lo, 1ull);
+        if (hi) atomicAdd_system(P.sig_hi, 1ull);
+      }
     };
     auto general_step = [&](int k) {
       const int gz = z0 + k;  // global streamed index
@@ -669,19 +723,41 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
         for (int q = 0; q < PPX; ++q) all = all && valid[q];
         cplx<R> *oTr = outT + int64_t(r) * P.pitch;
         cplx<R> *oAr = (LY::template writes_acc<MODE>()) ? outA + int64_t(r) * P.pitch : nullptr;
+        const int64_t fbytes = int64_t(nz) * P.plane * int64_t(sizeof(CT));  // output field extent
         if (all) {
 #pragma unroll
           for (int v = 0; v < PPX / VV::CPV; ++v) {
-            st_stream(reinterpret_cast<typename VV::T *>(oTr) + v, VV::join(oT + v * VV::CPV));
-            if (LY::template writes_acc<MODE>()) st_stream(reinterpret_cast<typename VV::T *>(oAr) + v, VV::join(oA + v * VV::CPV));
+            if (NLSE_STORE_OK(oTr + v * VV::CPV, VV::CPV, P.out_T, fbytes))
+              st_stream(reinterpret_cast<typename VV::T *>(oTr) + v, VV::join(oT + v * VV::CPV));
+            if (LY::template writes_acc<MODE>() && NLSE_STORE_OK(oAr + v * VV::CPV, VV::CPV, P.out_acc, fbytes))
+              st_stream(reinterpret_cast<typename VV::T *>(oAr) + v, VV::join(oA + v * VV::CPV));
           }
         } else {
 #pragma unroll
           for (int q = 0; q < PPX; ++q) {
             if (!valid[q]) continue;
-            oTr[q] = oT[q];
-            if (LY::template writes_acc<MODE>()) oAr[q] = oA[q];
+            if (NLSE_STORE_OK(oTr + q, 1, P.out_T, fbytes)) oTr[q] = oT[q];
+            if (LY::template writes_acc<MODE>() && NLSE_STORE_OK(oAr + q, 1, P.out_acc, fbytes)) oAr[q] = oA[q];
           }
+        }
+        (void)fbytes;
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+          CT *mb = side ? mirror_hi(k) : mirror_lo(k);
+          if (!mb) continue;
+          mb += int64_t(r) * P.pitch;
+          const CT *mbase = side ? P.mir_hi : P.mir_lo;
+          if (all) {
+#pragma unroll
+            for (int v = 0; v < PPX / VV::CPV; ++v)
+              if (NLSE_STORE_OK(mb + v * VV::CPV, VV::CPV, mbase, 2 * P.plane * int64_t(sizeof(CT))))
+                st_stream(reinterpret_cast<typename VV::T *>(mb) + v, VV::join(oT + v * VV::CPV));
+          } else {
+#pragma unroll
+            for (int q = 0; q < PPX; ++q)
+              if (valid[q] && NLSE_STORE_OK(mb + q, 1, mbase, 2 * P.plane * int64_t(sizeof(CT)))) mb[q] = oT[q];
+          }
+          (void)mbase;
         }
         // queue shift: (k-2, k-1, k+1) <- (k-1, k, k+2)
 #pragma unroll
@@ -693,6 +769,7 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
       }
       outT += P.plane;
       if (LY::template writes_acc<MODE>()) outA += P.plane;
+      signal(k);
       __syncwarp();
       if (NPA) {
         if (lane == 0) mbar_arrive(&emptyP[sp]);
@@ -832,12 +909,16 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
           }
         }
         using VV = V16<R>;
+        const int64_t fbytes = int64_t(nz) * plane * int64_t(sizeof(CT));
+        (void)fbytes;
 #pragma unroll
         for (int v = 0; v < PPX / VV::CPV; ++v) {
-          st_stream(reinterpret_cast<typename VV::T *>(outT + r * pitch) + v, VV::join(oT + v * VV::CPV));
-          if (LY::template writes_acc<MODE>())
+          if (NLSE_STORE_OK(outT + r * pitch + v * VV::CPV, VV::CPV, P.out_T, fbytes))
+            st_stream(reinterpret_cast<typename VV::T *>(outT + r * pitch) + v, VV::join(oT + v * VV::CPV));
+          if (LY::template writes_acc<MODE>() && NLSE_STORE_OK(outA + r * pitch + v * VV::CPV, VV::CPV, P.out_acc, fbytes))
             st_stream(reinterpret_cast<typename VV::T *>(outA + r * pitch) + v, VV::join(oA + v * VV::CPV));
         }
+
 #pragma unroll
         for (int q = 0; q < PPX; ++q) {
           qm2[r][q] = qm1[r][q];
@@ -864,20 +945,26 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
     // and the face rule on the boundary columns/rows; bit-identical to the general step
     // (P.lean bit 1: interior tiles, bit 2: face tiles; nlse2shoc_set_option LEAN_STEPS)
     const bool face_lean = (P.lean & 2) && DIMS == 3 && !inner_xy && P.vkind != 2 && x0 + TX <= nx && y0 + TY <= ny;
+    // lean planes: gz in [2, NZ-3], and not a plane the fused exchange mirrors to a neighbour
+    // (local 0, 1 with a lower peer, nz-2, nz-1 with an upper one: the general step stores
+    // those), clamped to this tile's chunk [kb, ke)
+    const int lean_lo = max(2 - z0, P.mir_lo ? 2 : 0), lean_hi = min(NZ - 2 - z0, P.mir_hi ? nz - 2 : nz);
     if (inner_xy && (P.lean & 1)) {
-      // lean planes: gz in [2, NZ-3], clamped to this tile's chunk [kb, ke)
-      const int l0 = min(ke, max(kb, 2 - z0)), l1 = max(l0, min(ke, NZ - 2 - z0));
+      const int l0 = min(ke, max(kb, lean_lo)), l1 = max(l0, min(ke, lean_hi));
       int k = kb;
       for (; k < l0; ++k) general_step(k);
       if (P.vkind == 2) {
         for (; k < l1; ++k) lean_step(k, std::true_type{}, std::false_type{});
       } else {
+        // unrolled by 3: the (k-2, k-1, k+1) register queue rotates by renaming instead of moves
+        // (C4 8.07 -> 7.98 ms/step, no spills; profiles/r02/ab_libs_c8.jsonl)
+#pragma unroll 3
         for (; k < l1; ++k) lean_step(k, std::false_type{}, std::false_type{});
       }
       for (; k < ke; ++k) general_step(k);
     } else if (DIMS == 3 && face_lean) {
       if constexpr (DIMS == 3) {
-        const int l0 = min(ke, max(kb, 2 - z0)), l1 = max(l0, min(ke, NZ - 2 - z0));
+        const int l0 = min(ke, max(kb, lean_lo)), l1 = max(l0, min(ke, lean_hi));
         int k = kb;
         for (; k < l0; ++k) general_step(k);
         for (; k < l1; ++k) lean_step(k, std::false_type{}, std::true_type{});
@@ -896,6 +983,14 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
       }
     }
     tcnt = tbase + uint32_t(ke - kb + 4);
+  }
+  if (P.cnt && threadIdx.x == 0) {
+    // fused exchange: the last CTA to finish advances this slab's epoch (every CTA has read it)
+    __threadfence();
+    if (atomicAdd(P.cnt + 3, 1ull) == gridDim.x - 1) {
+      atomicExch(P.cnt + 3, 0ull);
+      atomicAdd(P.cnt + 2, 1ull);
+    }
   }
 }
 

@@ -49,30 +49,39 @@ template <typename R> struct PlaneView {  // stencil-input planes incl. the 2-pl
   }
 };
 
+// Every two-kernel launch walks ZC consecutive planes per block (blockIdx.z = plane chunk):
+// one point per thread and plane, x / y neighbours through L1, the plane k+1 loads of one
+// iteration re-read from L1 as plane k's centre in the next.  (One block per plane meant
+// 1.8 M blocks of 256 points for C4, and block scheduling, not HBM, bounded the kernels.)
+constexpr int TWO_ZC = 16;
+
 // Kernel A: D on local planes [-1, nz] (index shifted by +1 in the D buffer).
 template <int DIMS, typename R>
 __global__ void __launch_bounds__(256) two_d_kernel(PlaneView<R> T, cplx<R> *__restrict__ D, const StageParams<R> P) {
   // 3D blocks cover 32 x 8 points of a plane, 1D/2D blocks 256 points of a row
   const int gx = DIMS == 3 ? blockIdx.x * 32 + (threadIdx.x & 31) : blockIdx.x * 256 + threadIdx.x;
   const int gy = DIMS == 3 ? blockIdx.y * 8 + (threadIdx.x >> 5) : 0;
-  const int lz = DIMS >= 2 ? int(blockIdx.z) - 1 : 0;
   if (gx >= P.nx || gy >= P.ny) return;
-  const int gz = P.z0 + lz;
-  if (DIMS >= 2 && (gz < 0 || gz >= P.NZ)) return;  // beyond a global face: never read
-  const cplx<R> *pl = T(DIMS >= 2 ? lz : 0);
+  const int z_begin = DIMS >= 2 ? int(blockIdx.z) * TWO_ZC - 1 : 0;
+  const int z_end = DIMS >= 2 ? min(z_begin + TWO_ZC, P.nz + 1) : 1;
   const int64_t o = int64_t(gy) * P.pitch + gx;
-  const cplx<R> c = pl[o];
-  const bool bnd = gx == 0 || gx == P.nx - 1 || (DIMS == 3 && (gy == 0 || gy == P.ny - 1)) ||
-                   (DIMS >= 2 && (gz == 0 || gz == P.NZ - 1));
-  cplx<R> d;
-  if (bnd) {
-    d = lambda_b(P, c, potential(P, gx, gy, lz));
-  } else {
-    d = d2(pl[o - 1], c, pl[o + 1], P.ihx2);
-    if (DIMS == 3) d = d + d2(pl[o - P.pitch], c, pl[o + P.pitch], P.ihy2);
-    if (DIMS >= 2) d = d + d2(T(lz - 1)[o], c, T(lz + 1)[o], P.ihz2);
+  for (int lz = z_begin; lz < z_end; ++lz) {
+    const int gz = P.z0 + lz;
+    if (DIMS >= 2 && (gz < 0 || gz >= P.NZ)) continue;  // beyond a global face: never read
+    const cplx<R> *pl = T(DIMS >= 2 ? lz : 0);
+    const cplx<R> c = pl[o];
+    const bool bnd = gx == 0 || gx == P.nx - 1 || (DIMS == 3 && (gy == 0 || gy == P.ny - 1)) ||
+                     (DIMS >= 2 && (gz == 0 || gz == P.NZ - 1));
+    cplx<R> d;
+    if (bnd) {
+      d = lambda_b(P, c, potential(P, gx, gy, lz));
+    } else {
+      d = d2(pl[o - 1], c, pl[o + 1], P.ihx2);
+      if (DIMS == 3) d = d + d2(pl[o - P.pitch], c, pl[o + P.pitch], P.ihy2);
+      if (DIMS >= 2) d = d + d2(T(lz - 1)[o], c, T(lz + 1)[o], P.ihz2);
+    }
+    D[(int64_t(DIMS >= 2 ? lz + 1 : 0)) * P.plane + o] = d;
   }
-  D[(int64_t(DIMS >= 2 ? lz + 1 : 0)) * P.plane + o] = d;
 }
 
 // Output of kernel B at local index g: L (MODE 5) or the Psi-space RK4 stage combine.
@@ -101,10 +110,11 @@ __global__ void __launch_bounds__(256) two_step2_kernel(PlaneView<R> T, const cp
   // 3D blocks cover 32 x 8 points of a plane, 1D/2D blocks 256 points of a row
   const int gx = DIMS == 3 ? blockIdx.x * 32 + (threadIdx.x & 31) : blockIdx.x * 256 + threadIdx.x;
   const int gy = DIMS == 3 ? blockIdx.y * 8 + (threadIdx.x >> 5) : 0;
-  const int lz = blockIdx.z;
   if (gx >= P.nx || gy >= P.ny) return;
-  const int gz = P.z0 + lz;
   const int64_t o = int64_t(gy) * P.pitch + gx;
+  const int z_end = DIMS >= 2 ? min(int(blockIdx.z + 1) * TWO_ZC, P.nz) : 1;
+  for (int lz = DIMS >= 2 ? int(blockIdx.z) * TWO_ZC : 0; lz < z_end; ++lz) {
+  const int gz = P.z0 + lz;
   const cplx<R> *pl = T(lz);
   const cplx<R> c = pl[o];
   const bool bnd = gx == 0 || gx == P.nx - 1 || (DIMS == 3 && (gy == 0 || gy == P.ny - 1)) ||
@@ -159,6 +169,7 @@ __global__ void __launch_bounds__(256) two_step2_kernel(PlaneView<R> T, const cp
     F = P.bc == 0 ? mk<R>(R(0), R(0)) : mk<R>(-(N * c.im), N * c.re);
   }
   two_store<R, MODE>(P, int64_t(lz) * P.plane + o, c, L, F, psi, acc);
+  }
 }
 
 template <int DIMS, typename R>
@@ -168,11 +179,11 @@ static cudaError_t launch_two_impl(int stage, const cplx<R> *in, const cplx<R> *
   PlaneView<R> T{in, lo ? lo : in, hi ? hi : in, P.nz, P.plane};
   dim3 blk(256);
   const int bx = DIMS == 3 ? (P.nx + 31) / 32 : (P.nx + 255) / 256;
-  dim3 ga(bx, DIMS == 3 ? (P.ny + 7) / 8 : 1, DIMS >= 2 ? P.nz + 2 : 1);
+  dim3 ga(bx, DIMS == 3 ? (P.ny + 7) / 8 : 1, DIMS >= 2 ? (P.nz + 2 + TWO_ZC - 1) / TWO_ZC : 1);
   two_d_kernel<DIMS, R><<<ga, blk, 0, st>>>(T, D, P);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  dim3 gb(bx, DIMS == 3 ? (P.ny + 7) / 8 : 1, DIMS >= 2 ? P.nz : 1);
+  dim3 gb(bx, DIMS == 3 ? (P.ny + 7) / 8 : 1, DIMS >= 2 ? (P.nz + TWO_ZC - 1) / TWO_ZC : 1);
   switch (stage) {
     case 1: two_step2_kernel<DIMS, R, M_S1><<<gb, blk, 0, st>>>(T, D, psi, acc, P, Q); break;
     case 2: two_step2_kernel<DIMS, R, M_S2><<<gb, blk, 0, st>>>(T, D, psi, acc, P, Q); break;
@@ -198,12 +209,14 @@ __global__ void __launch_bounds__(256) two_dms_kernel(PlaneView<R> T, cplx<R> *_
                                                       const StageParams<R> P) {
   const int gx = DIMS == 3 ? blockIdx.x * 32 + (threadIdx.x & 31) : blockIdx.x * 256 + threadIdx.x;
   const int gy = DIMS == 3 ? blockIdx.y * 8 + (threadIdx.x >> 5) : 0;
-  const int lz = DIMS >= 2 ? int(blockIdx.z) - 1 : 0;
   if (gx >= P.nx || gy >= P.ny) return;
-  const int gz = P.z0 + lz;
-  if (DIMS >= 2 && (gz < 0 || gz >= P.NZ)) return;
-  const cplx<R> *pl = T(DIMS >= 2 ? lz : 0);
   const int64_t o = int64_t(gy) * P.pitch + gx;
+  const int z_begin = DIMS >= 2 ? int(blockIdx.z) * TWO_ZC - 1 : 0;
+  const int z_end = DIMS >= 2 ? min(z_begin + TWO_ZC, P.nz + 1) : 1;
+  for (int lz = z_begin; lz < z_end; ++lz) {
+  const int gz = P.z0 + lz;
+  if (DIMS >= 2 && (gz < 0 || gz >= P.NZ)) continue;
+  const cplx<R> *pl = T(DIMS >= 2 ? lz : 0);
   const cplx<R> c = pl[o];
   // kernel axes present: x always, y in 3D, z (streamed) in 2D/3D
   const bool fx = gx == 0 || gx == P.nx - 1;
@@ -224,6 +237,7 @@ __global__ void __launch_bounds__(256) two_dms_kernel(PlaneView<R> T, cplx<R> *_
   D[g] = dx;
   if (DIMS == 3) D[Dfield + g] = dy;
   if (DIMS >= 2) D[(DIMS - 1) * Dfield + g] = dz;
+  }
 }
 
 template <int DIMS, typename R, int MODE>
@@ -232,10 +246,11 @@ __global__ void __launch_bounds__(256) two_step2ms_kernel(PlaneView<R> T, const 
                                                           const cplx<R> *__restrict__ acc, const StageParams<R> P) {
   const int gx = DIMS == 3 ? blockIdx.x * 32 + (threadIdx.x & 31) : blockIdx.x * 256 + threadIdx.x;
   const int gy = DIMS == 3 ? blockIdx.y * 8 + (threadIdx.x >> 5) : 0;
-  const int lz = blockIdx.z;
   if (gx >= P.nx || gy >= P.ny) return;
-  const int gz = P.z0 + lz;
   const int64_t o = int64_t(gy) * P.pitch + gx;
+  const int z_end = DIMS >= 2 ? min(int(blockIdx.z + 1) * TWO_ZC, P.nz) : 1;
+  for (int lz = DIMS >= 2 ? int(blockIdx.z) * TWO_ZC : 0; lz < z_end; ++lz) {
+  const int gz = P.z0 + lz;
   const cplx<R> c = T(lz)[o];
   const bool bnd = gx == 0 || gx == P.nx - 1 || (DIMS == 3 && (gy == 0 || gy == P.ny - 1)) ||
                    (DIMS >= 2 && (gz == 0 || gz == P.NZ - 1));
@@ -261,6 +276,7 @@ __global__ void __launch_bounds__(256) two_step2ms_kernel(PlaneView<R> T, const 
     F = P.bc == 0 ? mk<R>(R(0), R(0)) : mk<R>(-(N * c.im), N * c.re);
   }
   two_store<R, MODE>(P, int64_t(lz) * P.plane + o, c, L, F, psi, acc);
+  }
 }
 
 template <int DIMS, typename R>
@@ -270,11 +286,11 @@ static cudaError_t launch_two_ms_impl(int stage, const cplx<R> *in, const cplx<R
   PlaneView<R> T{in, lo ? lo : in, hi ? hi : in, P.nz, P.plane};
   dim3 blk(256);
   const int bx = DIMS == 3 ? (P.nx + 31) / 32 : (P.nx + 255) / 256;
-  dim3 ga(bx, DIMS == 3 ? (P.ny + 7) / 8 : 1, DIMS >= 2 ? P.nz + 2 : 1);
+  dim3 ga(bx, DIMS == 3 ? (P.ny + 7) / 8 : 1, DIMS >= 2 ? (P.nz + 2 + TWO_ZC - 1) / TWO_ZC : 1);
   two_dms_kernel<DIMS, R><<<ga, blk, 0, st>>>(T, D, Dfield, P);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  dim3 gb(bx, DIMS == 3 ? (P.ny + 7) / 8 : 1, DIMS >= 2 ? P.nz : 1);
+  dim3 gb(bx, DIMS == 3 ? (P.ny + 7) / 8 : 1, DIMS >= 2 ? (P.nz + TWO_ZC - 1) / TWO_ZC : 1);
   switch (stage) {
     case 1: two_step2ms_kernel<DIMS, R, M_S1><<<gb, blk, 0, st>>>(T, D, Dfield, psi, acc, P); break;
     case 2: two_step2ms_kernel<DIMS, R, M_S2><<<gb, blk, 0, st>>>(T, D, Dfield, psi, acc, P); break;

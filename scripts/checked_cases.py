@@ -1,6 +1,9 @@
-"""One small call of every kernel family, for compute-sanitizer (memcheck / racecheck /
-synccheck / initcheck): scripts/sanitize.sh runs this under each tool.  No oracle: the
-sanitizer checks memory and synchronisation, parity is tests/'s job."""
+"""One small call of every kernel family (fused 2D/3D incl. lean / face-lean / general steps,
+1D resident / tile / stream / MSD, two-kernel single- and multi-storage, stage pairs, CD,
+loopback shards with the fused exchange).  Run against the checked build
+(NLSE_LIB=paper_1109_1027_b200/libnlse2shoc_checked.so): it prints the number of out-of-range
+stores the range checks caught; tests/test_gpu_checked.py requires 0.  (compute-sanitizer is
+closed on the GPU pool, so these checks stand in for memcheck's store coverage.)"""
 import os
 import sys
 
@@ -70,4 +73,12 @@ run(3, (40, 30, 12), "dirichlet", "c64", scheme="cd")
 run(3, (70, 30, 24), "dirichlet", "c64", shard={"loopback": 3})
 run(3, (40, 33, 20), "lapzero", "c128", shard={"loopback": 2}, variant=1)
 run(2, (600, 40), "dirichlet", "c64", shard={"loopback": 4})
-print("all cases done", flush=True)
+run(3, (131, 51, 40), "lapzero", "c64", shard={"loopback": 8}, steps=3)
+run(3, (70, 67, 30), "dirichlet", "c128", shard={"loopback": 3}, variant=6, steps=3)
+run(3, (70, 30, 24), "dirichlet", "c64", shard={"loopback": 3}, opts=(("fused_exchange", 0),))
+from paper_1109_1027_b200 import _lib
+
+L = _lib.lib()
+v = L.nlse2shoc_checked_violations() if hasattr(L, "nlse2shoc_checked_violations") else -1
+print(f"library {L.nlse2shoc_version().decode()}", flush=True)
+print(f"violations {v}", flush=True)

@@ -125,3 +125,33 @@ def test_loopback_C4_seams_match_oracle():
     for (tlo, tcnt), gb in zip(T, got):
         want = H.oracle_crop_rk4(w, "c64", tlo, tcnt, dt, 10)
         H.compare(gb, want, 1e-5, f"C4 loopback P=8 10 steps, seam box {tlo}+{tcnt}")
+
+
+@pytest.mark.parametrize("variant", [0, 2, 6])
+@pytest.mark.parametrize("nslabs", [2, 3, 8])
+def test_fused_exchange_bitwise_and_one_launch_per_stage(nslabs, variant):
+    """Halo exchange fused into the stage kernels (loopback slabs are each other's peers): the
+    edge planes are stored straight into the neighbours' halo buffers and counted there, so a
+    step is 4 launches per slab and nothing else, bitwise equal to the NCCL-style exchange
+    (option FUSED_EXCHANGE = 0) and to the single slab; across calls the device-side epochs
+    keep the arrival counters consistent (second call, cached graph)."""
+    import paper_1109_1027_b200 as nl
+
+    w = configs.SMALL(3, (70, 33, 48), "dirichlet", dtype="c64", V="harmonic", noise=0.05)
+    psi0 = H.psi0_host(w, "c64")
+    res = {}
+    for fused in (1, 0):
+        S = nl.solver_from_work(w, "c64", shard={"loopback": nslabs})
+        if variant:
+            S.set_variant(variant)
+        S.set_option("fused_exchange", fused)
+        g = torch.from_numpy(psi0).cuda()
+        S.rk4(g, 1e-4, 3)
+        S.rk4(g, 1e-4, 3)
+        if fused:
+            assert S.last_launch_count == 4 * nslabs * 3
+        res[fused] = g.cpu()
+        S.close()
+    ref, _ = _run(w, "c64", None, variant, 6, 1e-4, psi0)
+    assert torch.equal(res[1], res[0])
+    assert np.array_equal(res[1].numpy().view(np.uint8), ref.view(np.uint8))

@@ -140,3 +140,36 @@ def test_bench_reference_arm_multirank_prints_once():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def _peer_worker(rank, ws, port, q):
+    import torch.distributed as dist
+
+    import paper_1109_1027_b200 as nl
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    mine = bytes([rank]) * 64
+    q.put((rank, nl.gather_peer_handles(mine)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ws", [2, 3])
+def test_gather_peer_handles_gloo(ws):
+    """Host side of the fused exchange (nlse2shoc_connect_peers): the all-gathered IPC handles
+    give each rank exactly its z-neighbours (None at the global faces)."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29650 + ws
+    ps = [ctx.Process(target=_peer_worker, args=(r, ws, port, q)) for r in range(ws)]
+    for p in ps:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(ws))
+    for p in ps:
+        p.join(timeout=60)
+    for r in range(ws):
+        lo, hi = got[r]
+        assert lo == (bytes([r - 1]) * 64 if r > 0 else None)
+        assert hi == (bytes([r + 1]) * 64 if r < ws - 1 else None)
