@@ -9,7 +9,9 @@
 
 namespace nlse {
 
-template <typename R> struct cplx { R re, im; };
+// Interleaved (re, im) pair with the alignment of the pair, so that one complex moves with
+// one 8-byte (complex64) or 16-byte (complex128) access (fields are element-aligned).
+template <typename R> struct alignas(2 * sizeof(R)) cplx { R re, im; };
 
 template <typename R> __device__ __forceinline__ cplx<R> mk(R r, R i) { return {r, i}; }
 template <typename R> __device__ __forceinline__ cplx<R> operator+(cplx<R> a, cplx<R> b) { return {a.re + b.re, a.im + b.im}; }

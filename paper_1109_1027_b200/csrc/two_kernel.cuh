@@ -64,23 +64,24 @@ __global__ void __launch_bounds__(256) two_d_kernel(PlaneView<R> T, cplx<R> *__r
   if (gx >= P.nx || gy >= P.ny) return;
   const int z_begin = DIMS >= 2 ? int(blockIdx.z) * TWO_ZC - 1 : 0;
   const int z_end = DIMS >= 2 ? min(z_begin + TWO_ZC, P.nz + 1) : 1;
-  const int64_t o = int64_t(gy) * P.pitch + gx;
-  for (int lz = z_begin; lz < z_end; ++lz) {
+  const int o = gy * int(P.pitch) + gx;  // in-plane offset (a plane has < 2^31 elements)
+  const int pitch = int(P.pitch);
+  const bool xy_bnd = gx == 0 || gx == P.nx - 1 || (DIMS == 3 && (gy == 0 || gy == P.ny - 1));
+  cplx<R> *Dp = D + (DIMS >= 2 ? int64_t(z_begin + 1) * P.plane : 0) + o;
+  for (int lz = z_begin; lz < z_end; ++lz, Dp += (DIMS >= 2 ? P.plane : 0)) {
     const int gz = P.z0 + lz;
     if (DIMS >= 2 && (gz < 0 || gz >= P.NZ)) continue;  // beyond a global face: never read
-    const cplx<R> *pl = T(DIMS >= 2 ? lz : 0);
-    const cplx<R> c = pl[o];
-    const bool bnd = gx == 0 || gx == P.nx - 1 || (DIMS == 3 && (gy == 0 || gy == P.ny - 1)) ||
-                     (DIMS >= 2 && (gz == 0 || gz == P.NZ - 1));
+    const cplx<R> *pl = T(DIMS >= 2 ? lz : 0) + o;
+    const cplx<R> c = pl[0];
     cplx<R> d;
-    if (bnd) {
+    if (xy_bnd || (DIMS >= 2 && (gz == 0 || gz == P.NZ - 1))) {
       d = lambda_b(P, c, potential(P, gx, gy, lz));
     } else {
-      d = d2(pl[o - 1], c, pl[o + 1], P.ihx2);
-      if (DIMS == 3) d = d + d2(pl[o - P.pitch], c, pl[o + P.pitch], P.ihy2);
+      d = d2(pl[-1], c, pl[1], P.ihx2);
+      if (DIMS == 3) d = d + d2(pl[-pitch], c, pl[pitch], P.ihy2);
       if (DIMS >= 2) d = d + d2(T(lz - 1)[o], c, T(lz + 1)[o], P.ihz2);
     }
-    D[(int64_t(DIMS >= 2 ? lz + 1 : 0)) * P.plane + o] = d;
+    *Dp = d;
   }
 }
 
@@ -111,64 +112,64 @@ __global__ void __launch_bounds__(256) two_step2_kernel(PlaneView<R> T, const cp
   const int gx = DIMS == 3 ? blockIdx.x * 32 + (threadIdx.x & 31) : blockIdx.x * 256 + threadIdx.x;
   const int gy = DIMS == 3 ? blockIdx.y * 8 + (threadIdx.x >> 5) : 0;
   if (gx >= P.nx || gy >= P.ny) return;
-  const int64_t o = int64_t(gy) * P.pitch + gx;
-  const int z_end = DIMS >= 2 ? min(int(blockIdx.z + 1) * TWO_ZC, P.nz) : 1;
-  for (int lz = DIMS >= 2 ? int(blockIdx.z) * TWO_ZC : 0; lz < z_end; ++lz) {
-  const int gz = P.z0 + lz;
-  const cplx<R> *pl = T(lz);
-  const cplx<R> c = pl[o];
-  const bool bnd = gx == 0 || gx == P.nx - 1 || (DIMS == 3 && (gy == 0 || gy == P.ny - 1)) ||
-                   (DIMS >= 2 && (gz == 0 || gz == P.NZ - 1));
-  const R V = potential(P, gx, gy, lz);
-  const R N = fma(P.s, norm2(c), -V);
-  cplx<R> L, F;
-  if (!bnd) {
-    const int64_t dz = DIMS >= 2 ? P.plane : 0;
-    const cplx<R> *Dc = D + (DIMS >= 2 ? int64_t(lz + 1) * P.plane : 0) + o;
-    const cplx<R> d0 = Dc[0];
-    cplx<R> sx = Dc[-1] + Dc[1];
-    cplx<R> sy = DIMS == 3 ? Dc[-P.pitch] + Dc[P.pitch] : mk<R>(R(0), R(0));
-    cplx<R> sz = DIMS >= 2 ? Dc[-dz] + Dc[dz] : mk<R>(R(0), R(0));
-    if (Q.iso) {
-      // -1/12 (sum of 2d D-neighbours - (16 - 2d) D) + 1/(6h^2) (edge-midpoints - 4 p Psi)
-      L = R(-1.0 / 12.0) * ((sx + sy + sz) - R(16 - 2 * DIMS) * d0);
-      if (DIMS >= 2) {
-        // edge midpoints minus 4 Psi per coordinate plane, the centre subtracted per plane
-        // (each group of four sums to 4 Psi exactly for a constant field, so L = 0 exactly)
-        const cplx<R> *zm = T(lz - 1) + o, *zp = T(lz + 1) + o;
-        cplx<R> e = axpy((zm[-1] + zm[1]) + (zp[-1] + zp[1]), R(-4), c);
-        if (DIMS == 3) {
-          e = e + axpy((pl[o - P.pitch - 1] + pl[o - P.pitch + 1]) + (pl[o + P.pitch - 1] + pl[o + P.pitch + 1]), R(-4), c);
-          e = e + axpy((zm[-P.pitch] + zm[P.pitch]) + (zp[-P.pitch] + zp[P.pitch]), R(-4), c);
+  const int o = gy * int(P.pitch) + gx;  // in-plane offset (a plane has < 2^31 elements)
+  const int pitch = int(P.pitch);
+  const bool xy_bnd = gx == 0 || gx == P.nx - 1 || (DIMS == 3 && (gy == 0 || gy == P.ny - 1));
+  const int z_begin = DIMS >= 2 ? int(blockIdx.z) * TWO_ZC : 0;
+  const int z_end = DIMS >= 2 ? min(z_begin + TWO_ZC, P.nz) : 1;
+  const int64_t dz = DIMS >= 2 ? P.plane : 0;
+  const cplx<R> *Dc = D + (DIMS >= 2 ? int64_t(z_begin + 1) * P.plane : 0) + o;
+  int64_t g = int64_t(z_begin) * P.plane + o;
+  for (int lz = z_begin; lz < z_end; ++lz, Dc += dz, g += dz) {
+    const int gz = P.z0 + lz;
+    const cplx<R> *pl = T(lz) + o;
+    const cplx<R> c = pl[0];
+    const R V = potential(P, gx, gy, lz);
+    const R N = fma(P.s, norm2(c), -V);
+    cplx<R> L, F;
+    if (!(xy_bnd || (DIMS >= 2 && (gz == 0 || gz == P.NZ - 1)))) {
+      const cplx<R> d0 = Dc[0];
+      cplx<R> sx = Dc[-1] + Dc[1];
+      cplx<R> sy = DIMS == 3 ? Dc[-pitch] + Dc[pitch] : mk<R>(R(0), R(0));
+      cplx<R> sz = DIMS >= 2 ? Dc[-dz] + Dc[dz] : mk<R>(R(0), R(0));
+      const cplx<R> *zm = DIMS >= 2 ? T(lz - 1) + o : pl, *zp = DIMS >= 2 ? T(lz + 1) + o : pl;
+      if (Q.iso) {
+        // -1/12 (sum of 2d D-neighbours - (16 - 2d) D) + 1/(6h^2) (edge-midpoints - 4 p Psi)
+        L = R(-1.0 / 12.0) * ((sx + sy + sz) - R(16 - 2 * DIMS) * d0);
+        if (DIMS >= 2) {
+          // edge midpoints minus 4 Psi per coordinate plane, the centre subtracted per plane
+          // (each group of four sums to 4 Psi exactly for a constant field, so L = 0 exactly)
+          cplx<R> e = axpy((zm[-1] + zm[1]) + (zp[-1] + zp[1]), R(-4), c);
+          if (DIMS == 3) {
+            e = e + axpy((pl[-pitch - 1] + pl[-pitch + 1]) + (pl[pitch - 1] + pl[pitch + 1]), R(-4), c);
+            e = e + axpy((zm[-pitch] + zm[pitch]) + (zp[-pitch] + zp[pitch]), R(-4), c);
+          }
+          L = L + Q.w2 * e;
         }
-        L = L + Q.w2 * e;
+      } else {
+        L = d0 - R(1.0 / 12.0) * ((sx + sy + sz) - R(2 * DIMS) * d0);
+        // sum_{d<e} (h_d^2+h_e^2)/12 delta_d^2 delta_e^2 Psi, each cross difference written as
+        // [corners - 2 (face neighbours of both axes) + 4 Psi] / (h_d^2 h_e^2)
+        auto cross = [&](cplx<R> corners, cplx<R> fd, cplx<R> fe, R w) {
+          return w * ((corners - R(2) * (fd + fe)) + R(4) * c);
+        };
+        const cplx<R> fx = pl[-1] + pl[1];
+        if (DIMS >= 2) {
+          const cplx<R> fz = zm[0] + zp[0];
+          L = L + cross((zm[-1] + zm[1]) + (zp[-1] + zp[1]), fx, fz, Q.cde[1]);
+          if (DIMS == 3) {
+            const cplx<R> fy = pl[-pitch] + pl[pitch];
+            L = L + cross((pl[-pitch - 1] + pl[-pitch + 1]) + (pl[pitch - 1] + pl[pitch + 1]), fx, fy, Q.cde[0]);
+            L = L + cross((zm[-pitch] + zm[pitch]) + (zp[-pitch] + zp[pitch]), fy, fz, Q.cde[2]);
+          }
+        }
       }
+      F = mk<R>(-fma(P.a, L.im, N * c.im), fma(P.a, L.re, N * c.re));
     } else {
-      L = d0 - R(1.0 / 12.0) * ((sx + sy + sz) - R(2 * DIMS) * d0);
-      // sum_{d<e} (h_d^2+h_e^2)/12 delta_d^2 delta_e^2 Psi, each cross difference written as
-      // [corners - 2 (face neighbours of both axes) + 4 Psi] / (h_d^2 h_e^2)
-      auto cross = [&](cplx<R> corners, cplx<R> fd, cplx<R> fe, R w) {
-        return w * ((corners - R(2) * (fd + fe)) + R(4) * c);
-      };
-      const cplx<R> fx = pl[o - 1] + pl[o + 1];
-      if (DIMS >= 2) {
-        const cplx<R> *zm = T(lz - 1) + o, *zp = T(lz + 1) + o;
-        const cplx<R> fz = zm[0] + zp[0];
-        L = L + cross((zm[-1] + zm[1]) + (zp[-1] + zp[1]), fx, fz, Q.cde[1]);
-        if (DIMS == 3) {
-          const cplx<R> fy = pl[o - P.pitch] + pl[o + P.pitch];
-          L = L + cross((pl[o - P.pitch - 1] + pl[o - P.pitch + 1]) + (pl[o + P.pitch - 1] + pl[o + P.pitch + 1]), fx,
-                        fy, Q.cde[0]);
-          L = L + cross((zm[-P.pitch] + zm[P.pitch]) + (zp[-P.pitch] + zp[P.pitch]), fy, fz, Q.cde[2]);
-        }
-      }
+      L = lambda_b(P, c, V);
+      F = P.bc == 0 ? mk<R>(R(0), R(0)) : mk<R>(-(N * c.im), N * c.re);
     }
-    F = mk<R>(-fma(P.a, L.im, N * c.im), fma(P.a, L.re, N * c.re));
-  } else {
-    L = lambda_b(P, c, V);
-    F = P.bc == 0 ? mk<R>(R(0), R(0)) : mk<R>(-(N * c.im), N * c.re);
-  }
-  two_store<R, MODE>(P, int64_t(lz) * P.plane + o, c, L, F, psi, acc);
+    two_store<R, MODE>(P, g, c, L, F, psi, acc);
   }
 }
 

@@ -3,6 +3,6 @@
 ROUNDS=${ROUNDS:-3}
 for r in $(seq $ROUNDS); do
   for L in $LIBS; do
-    NLSE_LIB=$PWD/$L AB_REPS=${AB_REPS:-3} timeout 300 python scripts/ab_options.py ${CFG// /:} -- ${SETS:-tile_schedule=2} 2>&1 | tail -1 | sed "s|^|{\"lib\": \"$L\", \"round\": $r, \"r\": |; s|\$|}|"
+    NLSE_LIB=$PWD/$L AB_REPS=${AB_REPS:-3} timeout 300 python scripts/ab_options.py ${CFG// /:} -- ${SETS:-tile_schedule=2} 2>&1 | grep "^{" | sed "s|^|{\"lib\": \"$L\", \"round\": $r, \"r\": |; s|\$|}|"
   done
 done

@@ -151,6 +151,10 @@ def compare(got, want, tol, what=""):
     box's largest |Psi| (catches errors confined to a few points, e.g. a wrong ghost on one
     tile edge); both must be <= tol.  Each comparison is appended to $PARITY_LOG (JSON lines)
     when that is set, so the margins can be reported."""
+    import os
+
+    node = os.environ.get("PYTEST_CURRENT_TEST", "").split(" ")[0]
+    what = what or node
     got = np.asarray(got, dtype=np.complex128)
     want = np.asarray(want, dtype=np.complex128)
     if not np.any(want):
@@ -161,7 +165,6 @@ def compare(got, want, tol, what=""):
     rel = rel_l2(got, want)
     mx = float(np.abs(got - want).max() / max(np.abs(want).max(), 1e-300))
     import json
-    import os
 
     path = os.environ.get("PARITY_LOG")
     if path:

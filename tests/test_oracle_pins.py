@@ -463,12 +463,15 @@ FIG1_SLOW = [("cd", 0.125), ("2shoc", 0.0625), ("2shoc", 0.03125)]
 def test_P6_fig1_msd_dark_soliton(scheme, h):
     """Fig. 1: co-moving dark soliton with the MSD boundary (`msdbc_ut`,
     `msdbc_lap`; readings R5 domain [-25.5, 31], R28 Lap_{b-1} = D_{b-1}).
-    The paper does not state its domain, so magnitudes are pinned to 0.5 % (the domain
-    reading moves them by ~0.1-0.3 %) and the convergence orders to 0.005."""
+    The paper does not state its domain, and the domain reading moves the magnitudes by a
+    few 0.1 %: measured deviations are <= 0.02 % (CD) and 0.12 / 0.21 / 0.28 % (2SHOC at h =
+    1/2, 1/4, 1/8), so the pins are 0.05 % (CD), 0.35 % (2SHOC) and 0.5 % for the slow fine
+    rows; the convergence orders are pinned to 0.005 (test_P6_fig1_orders)."""
     er, ei = run_exp1(h, scheme)
     gr, gi = _golden("fig1_1d.txt", scheme, h)
-    assert abs(er / float(gr) - 1) < 5e-3, (er, gr)
-    assert abs(ei / float(gi) - 1) < 5e-3, (ei, gi)
+    tol = 5e-3 if (scheme, h) in FIG1_SLOW else (5e-4 if scheme == "cd" else 3.5e-3)
+    assert abs(er / float(gr) - 1) < tol, (er, gr)
+    assert abs(ei / float(gi) - 1) < tol, (ei, gi)
 
 
 def test_P6_fig1_orders():
