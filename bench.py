@@ -249,8 +249,12 @@ def run_ours(args):
     if work["grid"]["dims"] == 1 and ws > 1:
         raise SystemExit("1D configs are replicas only (DESIGN.md §8): run --gpus 1")
     S = nl.solver_from_work(work, dtype, shard=shard)
-    if ws > 1 and args.exchange == "fused":
-        S.connect_peers()  # halo exchange fused into the stage kernels over CUDA IPC / NVLink
+    exchange = args.exchange
+    if ws > 1 and exchange == "fused":
+        try:
+            S.connect_peers()  # halo exchange fused into the stage kernels over CUDA IPC / NVLink
+        except Exception as e:  # no peer mapping: the NCCL exchange (validated below)
+            exchange = f"nccl (connect_peers failed: {str(e)[:120]})"
     ctype = torch.complex64 if dtype == "c64" else torch.complex128
     g = work["grid"]
     npts_global = int(np.prod(g["n"][:3]))
@@ -266,6 +270,21 @@ def run_ours(args):
     psi = host.cuda()
     kmax = S.stability_bound(psi)
     dt = 0.8 * kmax
+    if ws > 1 and exchange == "fused":
+        # the fused exchange must reproduce the NCCL exchange bit for bit on every rank (and no
+        # arrival wait may have timed out), else the timed run uses the NCCL exchange
+        a, b = psi.clone(), psi.clone()
+        S.rk4(a, dt, 2)
+        S.set_option("fused_exchange", 0)
+        S.rk4(b, dt, 2)
+        S.set_option("fused_exchange", 1)
+        ok = torch.tensor([1 if (torch.equal(torch.view_as_real(a), torch.view_as_real(b))
+                                 and S.exchange_timeouts == 0) else 0], device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            S.set_option("fused_exchange", 0)
+            exchange = "nccl (fused exchange failed its bitwise check against NCCL)"
+        del a, b
 
     def barrier():
         if dist is not None:
@@ -336,7 +355,7 @@ def run_ours(args):
             "dtype": "c64 (fp32 pairs)" if dtype == "c64" else "c128 (fp64 pairs)", "data": "synthetic",
             "config": {"workload": WORKLOADS[wl], "grid": g["n"][:dims], "bc": work["bc"],
                        "V": work["V"]["kind"], "dt": dt, "kmax": kmax,
-                       "parallelism": f"z-slab x{ws}, {args.exchange} halo exchange" if ws > 1 else "single GPU",
+                       "parallelism": f"z-slab x{ws}, {exchange} halo exchange" if ws > 1 else "single GPU",
                        "l2": f"inputs ({host.numel() * host.element_size() / 2**30:.2f} GiB per field per GPU) vs "
                              "L2 126 MB: no flush" + (" (C2: fields comparable to L2, DRAM bytes can fall "
                                                       "below algorithmic)" if wl == "C2" else "")},

@@ -120,6 +120,11 @@ nlse2shoc_status nlse2shoc_create_sharded(nlse2shoc_t *out, int dims, const int6
  *                 must connect before its next rk4 call; the binding's Solver.connect_peers()
  *                 gathers the handles with torch.distributed.                              */
 nlse2shoc_status nlse2shoc_ipc_handle(nlse2shoc_t, void *handle64);
+/* Fused exchange diagnostics: arrival waits that gave up after ~4 s (a neighbour that never
+ * arrived: ranks calling differently, or a dead rank) since create, summed over the handle's
+ * slabs; the kernel finishes instead of hanging, and the result of that call is invalid.
+ * Syncs the device.  -1 for a NULL handle, -2 on a CUDA error.                             */
+int64_t nlse2shoc_exchange_timeouts(nlse2shoc_t);
 nlse2shoc_status nlse2shoc_connect_peers(nlse2shoc_t, const void *lower64, const void *upper64);
 
 /* Single-GPU emulation of the z-slab sharding (2D/3D): one handle holding nslabs virtual

@@ -265,6 +265,11 @@ class Solver:
         nlse2shoc_check_finite(self._h, self._check(psi), stream)
 
     @property
+    def exchange_timeouts(self) -> int:
+        """Fused-exchange waits that gave up (0 in a correct run); syncs the device."""
+        return int(lib().nlse2shoc_exchange_timeouts(self._h))
+
+    @property
     def workspace_bytes(self) -> int:
         return int(lib().nlse2shoc_workspace_bytes(self._h))
 

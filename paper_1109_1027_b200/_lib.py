@@ -79,6 +79,9 @@ def lib():
             fn.restype = ctypes.c_int
         L.nlse2shoc_workspace_bytes.argtypes = [H]
         L.nlse2shoc_workspace_bytes.restype = ctypes.c_size_t
+        if hasattr(L, "nlse2shoc_exchange_timeouts"):
+            L.nlse2shoc_exchange_timeouts.argtypes = [H]
+            L.nlse2shoc_exchange_timeouts.restype = ctypes.c_int64
         L.nlse2shoc_last_launch_count.argtypes = [H]
         L.nlse2shoc_last_launch_count.restype = ctypes.c_int64
         L.nlse2shoc_strerror.argtypes = [ctypes.c_int]
@@ -154,7 +157,7 @@ EXPORTS = [
     "nlse2shoc_local_extent",
     "nlse2shoc_split", "nlse2shoc_workspace_bytes", "nlse2shoc_set_variant", "nlse2shoc_set_scheme", "nlse2shoc_set_option",
     "nlse2shoc_ipc_handle", "nlse2shoc_connect_peers",
-    "nlse2shoc_laplacian",
+    "nlse2shoc_exchange_timeouts", "nlse2shoc_laplacian",
     "nlse2shoc_rk4", "nlse2shoc_stability_bound", "nlse2shoc_check_finite", "nlse2shoc_last_launch_count",
     "nlse2shoc_strerror", "nlse2shoc_last_error", "nlse2shoc_version", "nlse2shoc_destroy",
     "nlse2shoc_set_allocator", "nlse2shoc_checked_violations",

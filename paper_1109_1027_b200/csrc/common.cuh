@@ -198,8 +198,20 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void wait_counter(const unsigned long long *p, unsigned long long target) {
-  while (ld_acquire_sys(p) < target) __nanosleep(128);
+// The wait is bounded (~4 s): a neighbour that never arrives (a rank that died, or calls that
+// differ between ranks) counts a timeout in *timeouts and lets the kernel finish instead of
+// hanging the GPU; nlse2shoc_exchange_timeouts() reports it.
+__device__ __forceinline__ void wait_counter(const unsigned long long *p, unsigned long long target,
+                                             unsigned long long *timeouts) {
+  uint32_t spins = 0;
+  // once a wait has timed out on this slab, later ones do not wait (the call is invalid)
+  while (ld_acquire_sys(p) < target && *reinterpret_cast<volatile unsigned long long *>(timeouts) == 0) {
+    __nanosleep(128);
+    if (++spins == (1u << 25)) {
+      atomicAdd(timeouts, 1ull);
+      break;
+    }
+  }
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 

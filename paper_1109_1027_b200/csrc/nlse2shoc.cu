@@ -1529,6 +1529,22 @@ nlse2shoc_status nlse2shoc_check_finite(nlse2shoc_t H, const void *psi, void *st
   return NLSE2SHOC_OK;
 }
 
+int64_t nlse2shoc_exchange_timeouts(nlse2shoc_t H) {
+  if (!H) return -1;
+  DeviceGuard dg(H->device);
+  if (cudaDeviceSynchronize() != cudaSuccess) return -2;
+  int64_t n = 0;
+  std::vector<nlse2shoc_t> hs = H->slabs;
+  if (hs.empty()) hs.push_back(H);
+  for (nlse2shoc_t S : hs) {
+    if (!S->cnt) continue;
+    unsigned long long v = 0;
+    if (cudaMemcpy(&v, S->cnt + 4, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess) return -2;
+    n += int64_t(v);
+  }
+  return n;
+}
+
 int64_t nlse2shoc_last_launch_count(nlse2shoc_t H) {
   if (!H) return -1;
   int64_t n = H->launches;

@@ -116,7 +116,8 @@ template <typename R> struct StageParams {
   // the producer waits until the counter that neighbour raises (cnt[0] lower, cnt[1] upper)
   // reaches 2 ncol e, e = this slab's fused-launch epoch (cnt[2]; kept on the device, so a
   // captured graph stays valid, and advanced by the CTA that finishes last, cnt[3] counting).
-  // cnt: this slab's {from below, from above, epoch, finished CTAs}.  All null: no fused exchange.
+  // cnt: this slab's {from below, from above, epoch, finished CTAs, wait timeouts}.  All null:
+  // no fused exchange.
   cplx<R> *mir_lo, *mir_hi;
   unsigned long long *sig_lo, *sig_hi;
   unsigned long long *cnt;
@@ -363,14 +364,14 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
             m = &tm_lo;
             pz = p + 2;
             if (need_lo) {  // fused exchange: the lower neighbour's edge planes have landed
-              wait_counter(P.cnt, arrivals);
+              wait_counter(P.cnt, arrivals, P.cnt + 4);
               need_lo = false;
             }
           } else if (p >= P.nz && P.has_hi_halo) {
             m = &tm_hi;
             pz = p - P.nz;
             if (need_hi) {
-              wait_counter(P.cnt + 1, arrivals);
+              wait_counter(P.cnt + 1, arrivals, P.cnt + 4);
               need_hi = false;
             }
           }

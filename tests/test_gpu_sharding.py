@@ -150,6 +150,7 @@ def test_fused_exchange_bitwise_and_one_launch_per_stage(nslabs, variant):
         S.rk4(g, 1e-4, 3)
         if fused:
             assert S.last_launch_count == 4 * nslabs * 3
+            assert S.exchange_timeouts == 0
         res[fused] = g.cpu()
         S.close()
     ref, _ = _run(w, "c64", None, variant, 6, 1e-4, psi0)
