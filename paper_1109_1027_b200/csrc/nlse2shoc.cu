@@ -352,15 +352,24 @@ static nlse2shoc_status launch_stream(nlse2shoc_t H, Field &in, const CUtensorMa
   // z-chunks: minimise rounds * (chunk length + priming cost).  3D: chunks of at most 64 planes
   // where possible — neighbouring tiles of a round then stay close in z and their halo reads
   // hit L2 (C4: 110-plane chunks 9.35 ms/step, 55-plane chunks 9.24).
+  // Dynamic schedule (P.sched): tiles are taken in order by whichever CTA is free, so the cost
+  // is the total work plus one tile of tail, ntiles (L + p) / G + (L + p), with p the priming
+  // cost in planes (measured: 2 for complex64, 4 for complex128 tiles; C4 as 8 slabs of 96
+  // planes 9.72 -> 9.46 ms/step with 24-plane chunks, C5W c64 2.13 -> 2.08).
   int best = 1, best_any = 1;
   double bestc = 1e300, bestc_any = 1e300;
   const int nzr = P.ze - P.zb;  // planes this launch computes
   for (int nc = 1; nc <= 256 && 4 * nc <= nzr + 3; ++nc) {
-    const double rounds = std::ceil(double(ncol) * nc / G0);
-    const double len = std::ceil(double(nzr) / nc) + 1.5;
-    const double c = rounds * len;
+    const double L = std::ceil(double(nzr) / nc);
+    double c;
+    if (P.sched) {
+      const double p = sizeof(R) == 4 ? 2.0 : 4.0;
+      c = double(ncol) * nc * (L + p) / G0 + (L + p);
+    } else {
+      c = std::ceil(double(ncol) * nc / G0) * (L + 1.5);
+    }
     if (c < bestc_any - 1e-9) { bestc_any = c; best_any = nc; }
-    if ((DIMS != 3 || len - 1.5 <= 64.0) && c < bestc - 1e-9) { bestc = c; best = nc; }
+    if ((DIMS != 3 || L <= 64.0) && c < bestc - 1e-9) { bestc = c; best = nc; }
   }
   if (bestc > 1e299) best = best_any;
   if (H->opt_zchunks > 0) best = std::min<int>(H->opt_zchunks, nzr);

@@ -156,3 +156,26 @@ def test_fused_exchange_bitwise_and_one_launch_per_stage(nslabs, variant):
     ref, _ = _run(w, "c64", None, variant, 6, 1e-4, psi0)
     assert torch.equal(res[1], res[0])
     assert np.array_equal(res[1].numpy().view(np.uint8), ref.view(np.uint8))
+
+
+def test_loopback_C5W_weak_P2_stated_steps_match_oracle():
+    """C5's weak-scaling configuration at P = 2 (768 x 768 x 384, the z-slab seam at 192) run
+    sharded with the fused exchange for its stated 50 steps: a box across the seam at a global
+    x-y corner and one at the far corner, against oracle crops (margin 400; a box at the
+    Gaussian's centre would need ~2 min of oracle time, C5W(P=1) covers it)."""
+    import paper_1109_1027_b200 as nl
+
+    w = configs.C5W(2)
+    g, kmax = H.gpu_field(w, "c64", with_kmax=True)
+    dt = 0.8 * kmax
+    S = nl.solver_from_work(w, "c64", shard={"loopback": 2})
+    S.rk4(g, dt, w["steps"])
+    assert S.exchange_timeouts == 0
+    T = [([0, 0, 184], [16, 16, 16]), ([752, 0, 368], [16, 16, 16])]
+    got = [g[H.sl(3, a, b)].cpu().numpy() for a, b in T]
+    S.close()
+    del g
+    torch.cuda.empty_cache()
+    for (tlo, tcnt), gb in zip(T, got):
+        want = H.oracle_crop_rk4(w, "c64", tlo, tcnt, dt, w["steps"])
+        H.compare(gb, want, 1e-5, f"C5W(P=2) loopback fused 50 steps, box {tlo}+{tcnt}")
