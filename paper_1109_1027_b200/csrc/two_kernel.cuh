@@ -68,20 +68,27 @@ __global__ void __launch_bounds__(256) two_d_kernel(PlaneView<R> T, cplx<R> *__r
   const int pitch = int(P.pitch);
   const bool xy_bnd = gx == 0 || gx == P.nx - 1 || (DIMS == 3 && (gy == 0 || gy == P.ny - 1));
   cplx<R> *Dp = D + (DIMS >= 2 ? int64_t(z_begin + 1) * P.plane : 0) + o;
+  // z register queue: the centre column at planes lz-1, lz, lz+1 (plane lz+1 is the only new
+  // centre load per plane; planes beyond a global face read a valid buffer and go unused)
+  cplx<R> cm = DIMS >= 2 ? T(z_begin - 1)[o] : mk<R>(R(0), R(0)), c0 = T(DIMS >= 2 ? z_begin : 0)[o];
   for (int lz = z_begin; lz < z_end; ++lz, Dp += (DIMS >= 2 ? P.plane : 0)) {
+    const cplx<R> cp = DIMS >= 2 ? T(lz + 1)[o] : c0;
     const int gz = P.z0 + lz;
-    if (DIMS >= 2 && (gz < 0 || gz >= P.NZ)) continue;  // beyond a global face: never read
     const cplx<R> *pl = T(DIMS >= 2 ? lz : 0) + o;
-    const cplx<R> c = pl[0];
-    cplx<R> d;
-    if (xy_bnd || (DIMS >= 2 && (gz == 0 || gz == P.NZ - 1))) {
-      d = lambda_b(P, c, potential(P, gx, gy, lz));
-    } else {
-      d = d2(pl[-1], c, pl[1], P.ihx2);
-      if (DIMS == 3) d = d + d2(pl[-pitch], c, pl[pitch], P.ihy2);
-      if (DIMS >= 2) d = d + d2(T(lz - 1)[o], c, T(lz + 1)[o], P.ihz2);
+    const cplx<R> c = c0;
+    if (!(DIMS >= 2 && (gz < 0 || gz >= P.NZ))) {  // beyond a global face: never read
+      cplx<R> d;
+      if (xy_bnd || (DIMS >= 2 && (gz == 0 || gz == P.NZ - 1))) {
+        d = lambda_b(P, c, potential(P, gx, gy, lz));
+      } else {
+        d = d2(pl[-1], c, pl[1], P.ihx2);
+        if (DIMS == 3) d = d + d2(pl[-pitch], c, pl[pitch], P.ihy2);
+        if (DIMS >= 2) d = d + d2(cm, c, cp, P.ihz2);
+      }
+      *Dp = d;
     }
-    *Dp = d;
+    cm = c0;
+    c0 = cp;
   }
 }
 
@@ -104,7 +111,7 @@ __device__ __forceinline__ void two_store(const StageParams<R> &P, int64_t g, cp
 
 // Kernel B: step 2 + F + stage combine (MODE 1-4) or L (MODE 5) on local planes [0, nz).
 template <int DIMS, typename R, int MODE>
-__global__ void __launch_bounds__(256) two_step2_kernel(PlaneView<R> T, const cplx<R> *__restrict__ D,
+__global__ void __launch_bounds__(256, 4) two_step2_kernel(PlaneView<R> T, const cplx<R> *__restrict__ D,
                                                          const cplx<R> *__restrict__ psi,
                                                          const cplx<R> *__restrict__ acc, const StageParams<R> P,
                                                          const TwoParams<R> Q) {
@@ -120,29 +127,45 @@ __global__ void __launch_bounds__(256) two_step2_kernel(PlaneView<R> T, const cp
   const int64_t dz = DIMS >= 2 ? P.plane : 0;
   const cplx<R> *Dc = D + (DIMS >= 2 ? int64_t(z_begin + 1) * P.plane : 0) + o;
   int64_t g = int64_t(z_begin) * P.plane + o;
+  const cplx<R> zero = mk<R>(R(0), R(0));
+  // z register queues (planes k-1, k, k+1): the Psi centre, the Psi "cross" neighbours
+  // (x-1, x+1, y-1, y+1) and the D centre; per plane only plane k+1's centre and cross, plane
+  // k's diagonals and D's in-plane neighbours are loaded (14 loads per point instead of 21 in
+  // 3D: the L1 pipe is what bounds this kernel).  Boundary threads skip the neighbour loads.
+  struct Cross { cplx<R> xm, xp, ym, yp; };
+  auto cross_at = [&](const cplx<R> *q) -> Cross {
+    if (xy_bnd) return {zero, zero, zero, zero};
+    return {q[-1], q[1], DIMS == 3 ? q[-pitch] : zero, DIMS == 3 ? q[pitch] : zero};
+  };
+  const cplx<R> *q0 = T(z_begin) + o;
+  cplx<R> cm = DIMS >= 2 ? T(z_begin - 1)[o] : zero, c0 = q0[0];
+  Cross xm_ = DIMS >= 2 ? cross_at(T(z_begin - 1) + o) : Cross{zero, zero, zero, zero}, x0_ = cross_at(q0);
+  cplx<R> dm = DIMS >= 2 ? Dc[-dz] : zero, d0 = Dc[0];
   for (int lz = z_begin; lz < z_end; ++lz, Dc += dz, g += dz) {
     const int gz = P.z0 + lz;
     const cplx<R> *pl = T(lz) + o;
-    const cplx<R> c = pl[0];
+    const cplx<R> *zp = DIMS >= 2 ? T(lz + 1) + o : pl;
+    const cplx<R> cp = DIMS >= 2 ? zp[0] : zero;
+    const Cross xp_ = DIMS >= 2 ? cross_at(zp) : Cross{zero, zero, zero, zero};
+    const cplx<R> dp = DIMS >= 2 ? Dc[dz] : zero;
+    const cplx<R> c = c0;
     const R V = potential(P, gx, gy, lz);
     const R N = fma(P.s, norm2(c), -V);
     cplx<R> L, F;
     if (!(xy_bnd || (DIMS >= 2 && (gz == 0 || gz == P.NZ - 1)))) {
-      const cplx<R> d0 = Dc[0];
       cplx<R> sx = Dc[-1] + Dc[1];
-      cplx<R> sy = DIMS == 3 ? Dc[-pitch] + Dc[pitch] : mk<R>(R(0), R(0));
-      cplx<R> sz = DIMS >= 2 ? Dc[-dz] + Dc[dz] : mk<R>(R(0), R(0));
-      const cplx<R> *zm = DIMS >= 2 ? T(lz - 1) + o : pl, *zp = DIMS >= 2 ? T(lz + 1) + o : pl;
+      cplx<R> sy = DIMS == 3 ? Dc[-pitch] + Dc[pitch] : zero;
+      cplx<R> sz = DIMS >= 2 ? dm + dp : zero;
       if (Q.iso) {
         // -1/12 (sum of 2d D-neighbours - (16 - 2d) D) + 1/(6h^2) (edge-midpoints - 4 p Psi)
         L = R(-1.0 / 12.0) * ((sx + sy + sz) - R(16 - 2 * DIMS) * d0);
         if (DIMS >= 2) {
           // edge midpoints minus 4 Psi per coordinate plane, the centre subtracted per plane
           // (each group of four sums to 4 Psi exactly for a constant field, so L = 0 exactly)
-          cplx<R> e = axpy((zm[-1] + zm[1]) + (zp[-1] + zp[1]), R(-4), c);
+          cplx<R> e = axpy((xm_.xm + xm_.xp) + (xp_.xm + xp_.xp), R(-4), c);
           if (DIMS == 3) {
             e = e + axpy((pl[-pitch - 1] + pl[-pitch + 1]) + (pl[pitch - 1] + pl[pitch + 1]), R(-4), c);
-            e = e + axpy((zm[-pitch] + zm[pitch]) + (zp[-pitch] + zp[pitch]), R(-4), c);
+            e = e + axpy((xm_.ym + xm_.yp) + (xp_.ym + xp_.yp), R(-4), c);
           }
           L = L + Q.w2 * e;
         }
@@ -153,23 +176,29 @@ __global__ void __launch_bounds__(256) two_step2_kernel(PlaneView<R> T, const cp
         auto cross = [&](cplx<R> corners, cplx<R> fd, cplx<R> fe, R w) {
           return w * ((corners - R(2) * (fd + fe)) + R(4) * c);
         };
-        const cplx<R> fx = pl[-1] + pl[1];
+        const cplx<R> fx = x0_.xm + x0_.xp;
         if (DIMS >= 2) {
-          const cplx<R> fz = zm[0] + zp[0];
-          L = L + cross((zm[-1] + zm[1]) + (zp[-1] + zp[1]), fx, fz, Q.cde[1]);
+          const cplx<R> fz = cm + cp;
+          L = L + cross((xm_.xm + xm_.xp) + (xp_.xm + xp_.xp), fx, fz, Q.cde[1]);
           if (DIMS == 3) {
-            const cplx<R> fy = pl[-pitch] + pl[pitch];
+            const cplx<R> fy = x0_.ym + x0_.yp;
             L = L + cross((pl[-pitch - 1] + pl[-pitch + 1]) + (pl[pitch - 1] + pl[pitch + 1]), fx, fy, Q.cde[0]);
-            L = L + cross((zm[-pitch] + zm[pitch]) + (zp[-pitch] + zp[pitch]), fy, fz, Q.cde[2]);
+            L = L + cross((xm_.ym + xm_.yp) + (xp_.ym + xp_.yp), fy, fz, Q.cde[2]);
           }
         }
       }
       F = mk<R>(-fma(P.a, L.im, N * c.im), fma(P.a, L.re, N * c.re));
     } else {
       L = lambda_b(P, c, V);
-      F = P.bc == 0 ? mk<R>(R(0), R(0)) : mk<R>(-(N * c.im), N * c.re);
+      F = P.bc == 0 ? zero : mk<R>(-(N * c.im), N * c.re);
     }
     two_store<R, MODE>(P, g, c, L, F, psi, acc);
+    cm = c0;
+    c0 = cp;
+    xm_ = x0_;
+    x0_ = xp_;
+    dm = d0;
+    d0 = dp;
   }
 }
 
