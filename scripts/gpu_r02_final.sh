@@ -9,5 +9,8 @@ timeout 300 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/f
 timeout 900 python scripts/perf_table.py > gpurun_out/final_perf_table.jsonl 2>&1; echo perf_rc=$?; cut -c1-200 gpurun_out/final_perf_table.jsonl
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv --log-file gpurun_out/final_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1; echo ncu_list_rc=$?
 python scripts/launches.py gpurun_out/final_launches.csv 452984832 | tee gpurun_out/final_launch_summary.txt
-timeout 1200 ncu --set full --import-source on --clock-control none -k regex:stage_stream_kernel --launch-skip 4 --launch-count 4 -o gpurun_out/final_step_full -f python scripts/one_step.py C4 c64 2 > /dev/null 2>&1; echo ncu_full_rc=$?
-python scripts/ncu_summary.py gpurun_out/final_step_full.ncu-rep > gpurun_out/final_stage_summary.txt; head -16 gpurun_out/final_stage_summary.txt
+# the full report is ~55 MB: keep it outside gpurun_out/ (64 MiB copy-back limit), bring back
+# the summary and the per-instruction source page of stage 1
+timeout 1200 ncu --set full --import-source on --clock-control none -k regex:stage_stream_kernel --launch-skip 4 --launch-count 4 -o /tmp/final_step_full -f python scripts/one_step.py C4 c64 2 > /dev/null 2>&1; echo ncu_full_rc=$?
+python scripts/ncu_summary.py /tmp/final_step_full.ncu-rep > gpurun_out/final_stage_summary.txt; head -16 gpurun_out/final_stage_summary.txt
+ncu -i /tmp/final_step_full.ncu-rep --page source --csv --print-source sass --kernel-name regex:"stage_stream_kernel<3, float, 6>" 2>/dev/null | gzip > gpurun_out/final_s1r_source.csv.gz

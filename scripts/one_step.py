@@ -1,6 +1,6 @@
 """One config, N RK4 steps with the given options (no CUDA graph, so every stage launch is a
 plain kernel launch): the command profiled by ncu for launch lists.
-  python scripts/one_step.py C4 c64 [steps] [opt=val ...]"""
+  python scripts/one_step.py C4 c64 [steps] [opt=val ...]   (loopback=P: virtual slabs)"""
 import os
 import sys
 
@@ -26,10 +26,13 @@ for z0 in range(0, nslow, 64):
     lo[dims - 1], cnt[dims - 1] = z0, min(64, nslow - z0)
     h = icgen.fill(w["ic"], g, dtype=np.complex64 if dtype == "c64" else np.complex128, lo=lo, cnt=cnt)
     psi[z0:z0 + cnt[dims - 1]].copy_(torch.from_numpy(h.reshape((cnt[dims - 1],) + shape[1:])))
-S = nl.solver_from_work(w, dtype)
+kvs = [kv.split("=") for kv in sys.argv[4:]]
+shard = {"loopback": int(v) for k, v in kvs if k == "loopback"} or None
+S = nl.solver_from_work(w, dtype, shard=shard)
 S.set_option("cuda_graph", 0)
-for kv in sys.argv[4:]:
-    k, v = kv.split("=")
+for k, v in kvs:
+    if k == "loopback":
+        continue
     if k == "variant":
         S.set_variant(int(v))
     else:
