@@ -462,12 +462,11 @@ template <typename R, int MODE>
 static nlse2shoc_status launch_line(nlse2shoc_t H, const void *in, const void *psi, const void *acc, StageParams<R> P,
                                     cudaStream_t st, const void *t3 = nullptr) {
   const int threads = 256;
-  // complex128 grids of >= 16 segments: the persistent bulk-copy ring (C2 0.187 -> 0.152 ms per
-  // step); smaller complex128 grids: the grid-stride kernel (L1 serves the stencil overlap;
-  // faster than shared-memory tiles, C2 0.191 vs 0.205-0.230 ms/step); complex64: tiles of 256
-  // points (C2 0.110 ms; 512 / 1024 / 2048-point tiles 0.128 / 0.119 / 0.115, grid-stride
-  // 0.125, the ring 0.113)
-  if (sizeof(R) == 8 && H->nx >= 16 * LineStream<R>::SEG) {
+  // Grids of >= 16 segments: the persistent bulk-copy ring, as many CTAs per SM as its shared
+  // memory allows (r2: C2 c64 0.0994 -> 0.0724 ms/step with 512-point segments and >= 3 CTAs
+  // per SM, c128 0.146 -> 0.130 from the occupancy-sized grid).  Smaller grids: complex128 the
+  // grid-stride kernel (L1 serves the stencil overlap), complex64 tiles of 256 points.
+  if (H->nx >= 16 * LineStream<R>::SEG) {
     static std::atomic<uint64_t> attr{0};
     const size_t smem = line_stream_smem<R, MODE>();
     if (attr_needed(attr)) {
@@ -475,7 +474,9 @@ static nlse2shoc_status launch_line(nlse2shoc_t H, const void *in, const void *p
       attr_done(attr);
     }
     const int64_t nseg = (H->nx + LineStream<R>::SEG - 1) / LineStream<R>::SEG;
-    const int grid = int(std::min<int64_t>(nseg, H->num_sms));
+    int occ = 1;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, line_stream_kernel<R, MODE>, LineStream<R>::NT, smem));
+    const int grid = int(std::min<int64_t>(nseg, int64_t(H->num_sms) * std::max(occ, 1)));
     line_stream_kernel<R, MODE><<<grid, LineStream<R>::NT, smem, st>>>(
         reinterpret_cast<const cplx<R> *>(in), reinterpret_cast<const cplx<R> *>(psi),
         reinterpret_cast<const cplx<R> *>(acc), reinterpret_cast<const cplx<R> *>(t3), P);

@@ -171,8 +171,12 @@ __global__ void __launch_bounds__(256) line_tile_kernel(const cplx<R> *__restric
 // the grid are loaded with plain loads (out-of-range halo entries are never read: the two
 // points at each end go through line_point on global memory).  Same arithmetic as
 // line_tile_kernel.
+// complex64: 512-point segments, 4 ring stages, >= 3 CTAs per SM (C2 c64 0.0994 -> 0.0724
+// ms/step against 1024-point segments with one CTA per SM: more loads in flight per SM).
+// (complex128 with 512-point segments, 4 stages, 2 CTAs per SM: the same 0.131 ms/step.)
 template <typename R> struct LineStream {
-  static constexpr int SEG = 1024, NS = sizeof(R) == 4 ? 4 : 3, NT = 256;
+  static constexpr int SEG = sizeof(R) == 4 ? 512 : 1024, NS = sizeof(R) == 4 ? 4 : 3, NT = 256;
+  static constexpr int MINB = sizeof(R) == 4 ? 3 : 1;  // CTAs per SM (launch bound)
 };
 template <typename R, int MODE> __host__ __device__ constexpr int line_npa() {
   return MODE == M_S4X ? 3 : ((MODE == M_S4R || MODE == M_S2 || MODE == M_S3 || MODE == M_S4) ? 2 :
@@ -184,7 +188,7 @@ template <typename R, int MODE> __host__ __device__ constexpr size_t line_stream
 }
 
 template <typename R, int MODE>
-__global__ void __launch_bounds__(256, 1) line_stream_kernel(const cplx<R> *__restrict__ Tin, const cplx<R> *__restrict__ psi,
+__global__ void __launch_bounds__(256, LineStream<R>::MINB) line_stream_kernel(const cplx<R> *__restrict__ Tin, const cplx<R> *__restrict__ psi,
                                                              const cplx<R> *__restrict__ acc, const cplx<R> *__restrict__ t3,
                                                              const StageParams<R> P) {
   using CT = cplx<R>;
