@@ -201,10 +201,11 @@ nlse2shoc_status nlse2shoc_set_scheme(nlse2shoc_t, int scheme);
  *  TILE_SCHEDULE [2] fused 2D/3D kernels: 0 = static (CTA b takes tiles b, b + G, ...),
  *                    1 = dynamic (tiles claimed in order from a counter in device memory,
  *                    so neighbouring tiles are streamed at nearly the same time whatever
- *                    each CTA's speed, and their halo re-reads hit L2), 2 = automatic:
- *                    dynamic in 3D (C4 8.83 -> 8.07 ms/step), static in 2D (C3: dynamic
- *                    is 17 % slower).  Dynamic needs the calls on a handle to be ordered
- *                    on one stream at a time (the counter is the handle's).
+ *                    each CTA's speed, and their halo re-reads hit L2), 2 = automatic =
+ *                    dynamic (C4 8.83 -> 8.07 ms/step; C3 c128 2.49 -> 2.38, c64 1.50 ->
+ *                    1.28 with the dynamic chunk model).  Dynamic needs the calls on a
+ *                    handle to be ordered on one stream at a time (the counter is the
+ *                    handle's).
  *  FUSED_EXCHANGE [1] sharded / loopback handles with peers: halo exchange fused into the
  *                    stage kernels (see nlse2shoc_connect_peers); 0 = the edge-first NCCL /
  *                    copy exchange (OVERLAP).

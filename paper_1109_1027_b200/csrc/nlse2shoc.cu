@@ -111,7 +111,7 @@ struct nlse2shoc_s {
   // execution-path options (nlse2shoc_set_option): results are the same up to the rounding
   // differences stated in include/nlse2shoc.h
   int opt_graph = 1, opt_overlap = 1, opt_resident = 1, opt_reverse = 1, opt_lean = 3, opt_zchunks = 0;
-  int opt_sched = -1;         // -1: automatic (dynamic in 3D, static in 2D)
+  int opt_sched = -1;         // -1: automatic (dynamic)
   unsigned *sched = nullptr;  // dynamic tile schedule counters {next tile, finished CTAs}
   // one instantiated RK4-step graph, reused by later calls with the same psi, dt and settings
   // (gen counts set_variant / set_scheme / set_option calls)
@@ -290,7 +290,7 @@ template <typename R> static void fill_params(nlse2shoc_t H, StageParams<R> &P) 
   P.inv_a = R(1.0 / H->a);
   P.bc = H->bc;
   P.lean = H->opt_lean;
-  P.sched = (H->opt_sched < 0 ? H->dims == 3 : H->opt_sched != 0) ? H->sched : nullptr;
+  P.sched = (H->opt_sched != 0) ? H->sched : nullptr;
   P.vkind = int(H->V.kind);
   if (H->V.kind == NLSE2SHOC_V_HARMONIC) {
     const R *t = reinterpret_cast<const R *>(H->vtab);
