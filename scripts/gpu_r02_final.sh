@@ -13,4 +13,4 @@ python scripts/launches.py gpurun_out/final_launches.csv 452984832 | tee gpurun_
 # the summary and the per-instruction source page of stage 1
 timeout 1200 ncu --set full --import-source on --clock-control none -k regex:stage_stream_kernel --launch-skip 4 --launch-count 4 -o /tmp/final_step_full -f python scripts/one_step.py C4 c64 2 > /dev/null 2>&1; echo ncu_full_rc=$?
 python scripts/ncu_summary.py /tmp/final_step_full.ncu-rep > gpurun_out/final_stage_summary.txt; head -16 gpurun_out/final_stage_summary.txt
-ncu -i /tmp/final_step_full.ncu-rep --page source --csv --print-source sass --kernel-name regex:"stage_stream_kernel<3, float, 6>" 2>/dev/null | gzip > gpurun_out/final_s1r_source.csv.gz
+ncu -i /tmp/final_step_full.ncu-rep --page source --csv --print-source sass 2>/dev/null | gzip > gpurun_out/final_stage_source.csv.gz
