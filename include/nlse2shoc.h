@@ -209,6 +209,10 @@ nlse2shoc_status nlse2shoc_set_scheme(nlse2shoc_t, int scheme);
  *  FUSED_EXCHANGE [1] sharded / loopback handles with peers: halo exchange fused into the
  *                    stage kernels (see nlse2shoc_connect_peers); 0 = the edge-first NCCL /
  *                    copy exchange (OVERLAP).
+ *  TAIL_CHUNKS  [1] fused 2D/3D kernels with the dynamic schedule: the z-chunk layout may
+ *                    end the streamed range on short chunks at both ends, so that the last
+ *                    tiles of a traversal (in either direction) are short and the CTAs
+ *                    finish together; 0 = equal chunks.  Bit-identical.
  * Single-slab and sharded rk4 calls keep their instantiated CUDA graph and replay it in
  * later calls with the same psi pointer and dt (any set_* call drops it).
  * EINVAL for an unknown option or a negative value.                                     */
@@ -220,7 +224,8 @@ typedef enum {
   NLSE2SHOC_OPT_LEAN_STEPS = 4,
   NLSE2SHOC_OPT_ZCHUNKS = 5,
   NLSE2SHOC_OPT_TILE_SCHEDULE = 6,
-  NLSE2SHOC_OPT_FUSED_EXCHANGE = 7
+  NLSE2SHOC_OPT_FUSED_EXCHANGE = 7,
+  NLSE2SHOC_OPT_TAIL_CHUNKS = 8
 } nlse2shoc_option;
 nlse2shoc_status nlse2shoc_set_option(nlse2shoc_t, int option, int64_t value);
 

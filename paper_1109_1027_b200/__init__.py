@@ -121,7 +121,7 @@ def nlse2shoc_check_finite(H, psi, stream=None):
 
 
 OPTIONS = {"cuda_graph": 0, "overlap": 1, "resident_1d": 2, "reverse_order": 3, "lean_steps": 4, "zchunks": 5,
-           "tile_schedule": 6, "fused_exchange": 7}
+           "tile_schedule": 6, "fused_exchange": 7, "tail_chunks": 8}
 
 
 def nlse2shoc_set_option(H, option, value: int):

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -75,6 +76,11 @@ struct Field {  // one pitched field of the local slab (+ its two halo buffers w
   CUtensorMap tm_in4{}, tm_ex{}, tm_ppt{};  // stage-pair kernel: halo-4 input, halo-2 Psi, acc tile
 };
 
+// z-chunk layout of a stage launch (StageParams nchunk / ns / ls / mlen).
+struct ZLayout {
+  int nchunk = 1, ns = 0, ls = 0, mlen = 1;
+};
+
 struct nlse2shoc_s {
   int dims = 0;
   int64_t N[3] = {1, 1, 1};  // global counts
@@ -112,6 +118,8 @@ struct nlse2shoc_s {
   // differences stated in include/nlse2shoc.h
   int opt_graph = 1, opt_overlap = 1, opt_resident = 1, opt_reverse = 1, opt_lean = 3, opt_zchunks = 0;
   int opt_sched = -1;         // -1: automatic (dynamic)
+  int opt_tail = 1;           // option TAIL_CHUNKS
+  std::map<uint64_t, ZLayout> zmemo;  // z-chunk layouts chosen so far (zlayout_dynamic)
   unsigned *sched = nullptr;  // dynamic tile schedule counters {next tile, finished CTAs}
   // one instantiated RK4-step graph, reused by later calls with the same psi, dt and settings
   // (gen counts set_variant / set_scheme / set_option calls)
@@ -335,6 +343,54 @@ static int zchunks_normalised(int n, int nchunk) {
   return (n + L - 1) / L;
 }
 
+// Dynamic tile schedule: choose the middle chunk count nm and the short end chunks (ns of ls
+// planes at each end) minimising  ncol * (planes + chunks * p) / G + tail,  where the tail is
+// one middle tile (mlen + p) unless the traversal ends on short chunk rows, which absorb it:
+// max(ls + p, mlen + p - S / G), S = the short-tile work at the end of the order.  (The
+// kernel's fused-exchange order runs chunks 0 and nchunk-1 first, so it ends on ns - 1 short
+// rows; forward and reversed traversals end on ns.)  Middle chunks at most maxl planes when
+// that is possible.  Memoised per handle (the search is ~40k evaluations).
+static ZLayout zlayout_dynamic(nlse2shoc_t H, int nzr, int ncol, int G, double p, int maxl, bool fused_order) {
+  const int tail = H->opt_tail;
+  const uint64_t key = (uint64_t(nzr) << 40) ^ (uint64_t(ncol) << 20) ^ (uint64_t(G) << 4) ^
+                       (uint64_t(p == 2.0) << 3) ^ (uint64_t(maxl == 64) << 2) ^ (uint64_t(fused_order) << 1) ^
+                       uint64_t(tail != 0);
+  auto it = H->zmemo.find(key);
+  if (it != H->zmemo.end()) return it->second;
+  static const int NS[] = {0, 1, 2, 3, 4, 6, 8, 12, 16, 24, 32, 48, 64};
+  static const int LS[] = {1, 2, 3, 4, 6, 8, 12, 16, 24, 32};
+  ZLayout best, best_any;
+  double bestc = 1e300, bestc_any = 1e300;
+  for (int ns : NS) {
+    if (ns > 0 && !tail) break;
+    for (int ls : LS) {
+      if (ns == 0 && ls > 1) break;
+      const int mid = nzr - 2 * ns * (ns ? ls : 0);
+      if (mid < 1) break;
+      for (int nm = 1; nm <= 256 && 4 * nm <= mid + 3; ++nm) {
+        const int mlen = (mid + nm - 1) / nm;
+        const int nme = (mid + mlen - 1) / mlen;  // non-empty middle chunks
+        if (nme != nm) continue;
+        const double work = double(ncol) * (mid + nme * p + 2.0 * ns * (ls + p)) / G;
+        const int send = ns == 0 ? 0 : (fused_order && nme + 2 * ns >= 3 ? ns - 1 : ns);
+        double tl = mlen + p;
+        if (send > 0) tl = std::max(double(ls) + p, mlen + p - double(ncol) * send * (ls + p) / G);
+        const double c = work + tl;
+        ZLayout z;
+        z.nchunk = nme + 2 * ns;
+        z.ns = ns;
+        z.ls = ns ? ls : 0;
+        z.mlen = mlen;
+        if (c < bestc_any - 1e-9) { bestc_any = c; best_any = z; }
+        if (mlen <= maxl && c < bestc - 1e-9) { bestc = c; best = z; }
+      }
+    }
+  }
+  if (bestc > 1e299) best = best_any;
+  H->zmemo[key] = best;
+  return best;
+}
+
 template <int DIMS, typename R, int MODE>
 static nlse2shoc_status launch_stream(nlse2shoc_t H, Field &in, const CUtensorMap *tm_psi, const CUtensorMap *tm_acc,
                                       StageParams<R> P, cudaStream_t st, const CUtensorMap *tm_t3 = nullptr) {
@@ -353,29 +409,37 @@ static nlse2shoc_status launch_stream(nlse2shoc_t H, Field &in, const CUtensorMa
   // where possible — neighbouring tiles of a round then stay close in z and their halo reads
   // hit L2 (C4: 110-plane chunks 9.35 ms/step, 55-plane chunks 9.24).
   // Dynamic schedule (P.sched): tiles are taken in order by whichever CTA is free, so the cost
-  // is the total work plus one tile of tail, ntiles (L + p) / G + (L + p), with p the priming
-  // cost in planes (measured: 2 for complex64, 4 for complex128 tiles; C4 as 8 slabs of 96
-  // planes 9.72 -> 9.46 ms/step with 24-plane chunks, C5W c64 2.13 -> 2.08).
-  int best = 1, best_any = 1;
-  double bestc = 1e300, bestc_any = 1e300;
+  // is the total work plus the tail, with p the priming cost in planes per tile (measured: 2 for
+  // complex64, 4 for complex128 tiles; C4 as 8 slabs of 96 planes 9.72 -> 9.46 ms/step with
+  // 24-plane chunks, C5W c64 2.13 -> 2.08).  The tail is one tile unless the traversal ends on
+  // short chunks (option TAIL_CHUNKS: ns chunks of ls planes at each end of the range, see
+  // zlayout_dynamic), which then only have to outlast the last long tile.
   const int nzr = P.ze - P.zb;  // planes this launch computes
-  for (int nc = 1; nc <= 256 && 4 * nc <= nzr + 3; ++nc) {
-    const double L = std::ceil(double(nzr) / nc);
-    double c;
-    if (P.sched) {
-      const double p = sizeof(R) == 4 ? 2.0 : 4.0;
-      c = double(ncol) * nc * (L + p) / G0 + (L + p);
-    } else {
-      c = std::ceil(double(ncol) * nc / G0) * (L + 1.5);
+  ZLayout zl;
+  if (H->opt_zchunks > 0) {
+    zl.nchunk = std::max(1, zchunks_normalised(nzr, std::min<int>(H->opt_zchunks, nzr)));
+    zl.mlen = (nzr + zl.nchunk - 1) / zl.nchunk;
+  } else if (P.sched) {
+    const bool fused_order = P.cnt != nullptr;  // the kernel's edge-chunks-first order
+    zl = zlayout_dynamic(H, nzr, ncol, G0, sizeof(R) == 4 ? 2.0 : 4.0, DIMS == 3 ? 64 : 1 << 30, fused_order);
+  } else {
+    int best = 1, best_any = 1;
+    double bestc = 1e300, bestc_any = 1e300;
+    for (int nc = 1; nc <= 256 && 4 * nc <= nzr + 3; ++nc) {
+      const double L = std::ceil(double(nzr) / nc);
+      const double c = std::ceil(double(ncol) * nc / G0) * (L + 1.5);
+      if (c < bestc_any - 1e-9) { bestc_any = c; best_any = nc; }
+      if ((DIMS != 3 || L <= 64.0) && c < bestc - 1e-9) { bestc = c; best = nc; }
     }
-    if (c < bestc_any - 1e-9) { bestc_any = c; best_any = nc; }
-    if ((DIMS != 3 || L <= 64.0) && c < bestc - 1e-9) { bestc = c; best = nc; }
+    if (bestc > 1e299) best = best_any;
+    zl.nchunk = std::max(1, zchunks_normalised(nzr, best));
+    zl.mlen = (nzr + zl.nchunk - 1) / zl.nchunk;
   }
-  if (bestc > 1e299) best = best_any;
-  if (H->opt_zchunks > 0) best = std::min<int>(H->opt_zchunks, nzr);
-  best = std::max(1, zchunks_normalised(nzr, best));
-  P.nchunk = best;
-  P.ntiles = ncol * best;
+  P.nchunk = zl.nchunk;
+  P.ns = zl.ns;
+  P.ls = zl.ls;
+  P.mlen = zl.mlen;
+  P.ntiles = ncol * zl.nchunk;
   const int G = std::min(G0, P.ntiles);
   P.in_T = reinterpret_cast<const cplx<R> *>(in.ptr);
   const CUtensorMap *lo = P.has_lo_halo ? &in.tm_lo : &in.tm;
@@ -1404,6 +1468,7 @@ nlse2shoc_status nlse2shoc_set_option(nlse2shoc_t H, int option, int64_t value) 
     case NLSE2SHOC_OPT_ZCHUNKS: H->opt_zchunks = v; break;
     case NLSE2SHOC_OPT_TILE_SCHEDULE: H->opt_sched = v >= 2 ? -1 : v; break;
     case NLSE2SHOC_OPT_FUSED_EXCHANGE: H->opt_fused = v != 0; break;
+    case NLSE2SHOC_OPT_TAIL_CHUNKS: H->opt_tail = v != 0; break;
     default: return fail(NLSE2SHOC_EINVAL, "unknown option");
   }
   ++H->gen;

@@ -96,6 +96,10 @@ template <typename R> struct StageParams {
   int lo_face, hi_face;  // streamed-axis ends are global faces (1) or shard seams (0)
   int has_lo_halo, has_hi_halo;
   int ncx, ncy, nchunk;  // tile grid: columns in x, in y, z-chunks
+  // z-chunk layout: ns chunks of ls planes at each end of [zb, ze), the nchunk - 2 ns middle
+  // chunks mlen planes each (the last one ragged).  Short end chunks are the last tiles of a
+  // traversal in either direction, so the CTAs finish within one short tile of each other.
+  int ns, ls, mlen;
   int ntiles;
   int64_t pitch;         // elements per x-row (all buffers)
   int64_t plane;         // elements per plane = pitch * ny
@@ -306,7 +310,19 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
   __syncthreads();
 
   const int G = gridDim.x;
-  const int chunk_len = (P.ze - P.zb + P.nchunk - 1) / P.nchunk;
+  // planes [kb, ke) of chunk c (layout: StageParams ns / ls / mlen)
+  auto chunk_range = [&](int c, int &kb, int &ke) {
+    if (c < P.ns) {
+      kb = P.zb + c * P.ls;
+      ke = kb + P.ls;
+    } else if (c >= P.nchunk - P.ns) {
+      ke = P.ze - (P.nchunk - 1 - c) * P.ls;
+      kb = ke - P.ls;
+    } else {
+      kb = P.zb + P.ns * P.ls + (c - P.ns) * P.mlen;
+      ke = min(P.ze - P.ns * P.ls, kb + P.mlen);
+    }
+  };
   const int ncol = P.ncx * P.ncy;
   // fused exchange: the two edge chunks (the planes the neighbours wait for) go first
   auto chunk_of = [&](int i) { return (!P.cnt || P.nchunk < 3) ? i : (i == 0 ? 0 : (i == 1 ? P.nchunk - 1 : i - 1)); };
@@ -352,7 +368,8 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
         const int tt = P.rev ? P.ntiles - 1 - t : t;  // reversed order: read the L2-resident tail first
         const int chunk = chunk_of(tt / ncol), col = tt % ncol;
         const int x0 = (col % P.ncx) * TX, y0 = (col / P.ncx) * TY;
-        const int kb = P.zb + chunk * chunk_len, ke = min(P.ze, kb + chunk_len);
+        int kb, ke;
+        chunk_range(chunk, kb, ke);
         bool need_lo = P.cnt && P.wait_lo, need_hi = P.cnt && P.wait_hi;
         auto produceT = [&](int p) {
           const uint32_t slot = tcnt % RT, par = (tcnt / RT) & 1;
@@ -474,7 +491,8 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
     const int tt = P.rev ? P.ntiles - 1 - t : t;
     const int chunk = chunk_of(tt / ncol), col = tt % ncol;
     const int x0 = (col % P.ncx) * TX, y0 = (col / P.ncx) * TY;
-    const int kb = P.zb + chunk * chunk_len, ke = min(P.ze, kb + chunk_len);
+    int kb, ke;
+    chunk_range(chunk, kb, ke);
     const uint32_t tbase = tcnt;  // ring counter of plane kb-2
     auto tslot = [&](int p) -> CT * { return ring + size_t((tbase + uint32_t(p - kb + 2)) % RT) * LY::SLOT; };
     auto twait = [&](int p) {

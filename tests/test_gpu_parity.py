@@ -512,7 +512,7 @@ def test_zchunk_counts_bit_identical(nz, chunks):
             assert torch.equal(g.cpu(), ref)
 
 
-@pytest.mark.parametrize("option", ["cuda_graph", "reverse_order"])
+@pytest.mark.parametrize("option", ["cuda_graph", "reverse_order", "tail_chunks"])
 def test_path_options_bit_identical(option):
     w = _small(3, (70, 30, 20), "lapzero", "c64", "harmonic")
     psi = H.psi0_host(w, "c64")
@@ -537,6 +537,28 @@ def test_V_array_is_validated():
         with pytest.raises(ValueError):
             nl.solver_from_work(w, "c128", V_array=bad)
     nl.solver_from_work(w, "c128", V_array=good).close()
+
+
+@pytest.mark.parametrize("dims,n,dtype,shard", [(3, (70, 30, 131), "c64", None), (3, (40, 33, 97), "c128", None),
+                                                (3, (70, 30, 131), "c64", {"loopback": 3}),
+                                                (2, (1100, 517), "c128", None), (2, (2100, 300), "c64", None)])
+def test_tail_chunks_bit_identical(dims, n, dtype, shard):
+    """TAIL_CHUNKS (short z-chunks at both ends of the streamed range) changes which CTA
+    computes a plane and in which order, nothing else: on and off give the same bits, for
+    single slabs, loopback slabs with the fused exchange, and the 2D row kernel."""
+    import paper_1109_1027_b200 as nl
+
+    w = _small(dims, n, "dirichlet", dtype, "harmonic")
+    psi = H.psi0_host(w, dtype)
+    res = []
+    for v in (1, 0):
+        S = nl.solver_from_work(w, dtype, shard=shard)
+        S.set_option("tail_chunks", v)
+        g = _dev(psi)
+        S.rk4(g, 1e-4, 5)
+        res.append(g.cpu())
+        S.close()
+    assert torch.equal(res[0], res[1])
 
 
 @pytest.mark.parametrize("shard", [None, {"loopback": 3}])
