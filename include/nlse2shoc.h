@@ -144,6 +144,28 @@ nlse2shoc_status nlse2shoc_split(int64_t n_slow, int nranks, int rank, int64_t *
 /* Device bytes the handle allocated (workspace + halos + tables). */
 size_t nlse2shoc_workspace_bytes(nlse2shoc_t);
 
+/* Caller-owned stage workspace (SURVEY §8(b) "optional: torch-owned").  The three stage
+ * fields of the RK4 combine (T_A, T_B, acc) are placed in `dev` (device memory
+ * of the handle's device, 256-byte aligned, at least nlse2shoc_stage_workspace_bytes(H) =
+ * 3 fields each rounded up to 256 B); the handle frees the ones it allocated at create and
+ * never frees `dev`, which the caller keeps alive until destroy or the next set_workspace.
+ * Several handles of the same size that never run concurrently may share one workspace.
+ * Syncs the device.  EINVAL: NULL / misaligned / too small / not device memory of this
+ * device; EUNSUPPORTED for loopback handles (their slabs own their workspaces).          */
+size_t nlse2shoc_stage_workspace_bytes(nlse2shoc_t);
+nlse2shoc_status nlse2shoc_set_workspace(nlse2shoc_t, void *dev, size_t bytes);
+
+/* The layout the kernels use in place (SURVEY §8(b) "optional zero-copy Psi"): pitch[0] =
+ * elements per x-row, pitch[1] = elements per plane (2D: per row), pitch[2] = elements of the
+ * local field; offset[] = 0 — there are no ghost layers in memory (ghost values are formed on
+ * chip).  pitch[0] equals N_x except for complex64 with odd N_x in 2D/3D, whose
+ * rows are padded to a whole 16-byte vector: nlse2shoc_rk4 stages such a dense Psi through a
+ * pitched copy (2 field passes per call), and nlse2shoc_rk4_padded takes Psi already in this
+ * layout (16-byte aligned; the pad element of each row is ignored and left untouched) and
+ * skips the copy.  For every other handle the two calls are the same.                    */
+nlse2shoc_status nlse2shoc_padded_layout(nlse2shoc_t, int64_t pitch[3], int64_t offset[3]);
+nlse2shoc_status nlse2shoc_rk4_padded(nlse2shoc_t, void *psi_padded, double dt, int64_t nsteps, void *stream);
+
 /* 0 = FUSED (default): one kernel per RK4 stage computes the whole 2SHOC Laplacian (both
  *     steps, D never stored), the RHS and the RK4 stage combine, 13 field transfers per
  *     point-step, in the write-light form (= variant 5).
@@ -154,6 +176,13 @@ size_t nlse2shoc_workspace_bytes(nlse2shoc_t);
  * 6 = FUSED_RECON: stage 1 stores only T_A = Psi + k/2 K1, stage 2 forms acc = Psi + (T_A -
  *     Psi)/3 + k/3 K2, stage 3 stores only T_A = Psi + k K3, stage 4 forms Psi' = acc +
  *     (T_A - Psi)/3 + k/6 K4.
+ * 7 = FUSED_CARRIED (12 transfers per point-step, the fewest with one pass per stage:
+ *     every stage reads its stencil input and writes its output, stages 2-3 read Psi, one
+ *     carried field is written once and read once): stage 2 also stores Q = 3 acc - Psi =
+ *     [2 Psi + (T_A - Psi)] + k K2, stage 3 writes T_C = Psi + k K3 over T_A, and stage 4
+ *     forms Psi' = (Q + T_C + k/2 K4)/3 from T_C and Q alone, with the sum carried exactly and
+ *     a correctly rounded division by 3 (one rounding of size ulp(Psi) per step; stationary
+ *     fields and Dirichlet boundary values are reproduced to the bit).
  * 1 = TWO_KERNEL: the paper's single-storage scheme (`2d2shocs1/2`, `3d2shocs`):
  *     kernel A stores D = sum_d delta_d^2 Psi (D_b = lambda_b), kernel B applies step 2 +
  *     RHS + combine.  One more field of workspace (allocated on first use).

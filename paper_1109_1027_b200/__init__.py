@@ -258,6 +258,43 @@ class Solver:
     def rk4(self, psi, dt, nsteps, stream=None):
         return nlse2shoc_rk4(self._h, self._check(psi), dt, nsteps, stream)
 
+    @property
+    def padded_layout(self):
+        """(pitch, offset): elements per x-row / per plane / per local field the kernels use in
+        place, and the (zero) ghost offsets (nlse2shoc_padded_layout)."""
+        pitch, off = (ctypes.c_int64 * 3)(), (ctypes.c_int64 * 3)()
+        check(lib().nlse2shoc_padded_layout(self._h, pitch, off), "padded_layout")
+        return list(pitch), list(off)
+
+    def rk4_padded(self, psi, dt, nsteps, stream=None):
+        """rk4 on a Psi already in padded_layout (rows of pitch[0] elements): a CUDA tensor
+        whose last dimension is pitch[0] (the pad column is ignored and left untouched)."""
+        import torch
+
+        pitch, _ = self.padded_layout
+        want = torch.complex64 if self.dtype == "c64" else torch.complex128
+        shape = tuple(self.local_shape[:-1]) + (pitch[0],)
+        if (not isinstance(psi, torch.Tensor) or not psi.is_cuda or psi.dtype != want or not psi.is_contiguous()
+                or tuple(psi.shape) != shape):
+            raise ValueError(f"psi must be a contiguous CUDA {want} tensor of shape {shape}")
+        st = _stream(stream)
+        check(lib().nlse2shoc_rk4_padded(self._h, psi.data_ptr(), float(dt), int(nsteps), st), "rk4_padded")
+        return psi
+
+    @property
+    def stage_workspace_bytes(self) -> int:
+        return int(lib().nlse2shoc_stage_workspace_bytes(self._h))
+
+    def set_workspace(self, buf):
+        """Place the three stage fields in the caller's CUDA tensor (any dtype, at least
+        stage_workspace_bytes, 256-byte aligned); the Solver keeps a reference to it."""
+        import torch
+
+        if not isinstance(buf, torch.Tensor) or not buf.is_cuda or not buf.is_contiguous():
+            raise ValueError("workspace must be a contiguous CUDA tensor")
+        check(lib().nlse2shoc_set_workspace(self._h, buf.data_ptr(), buf.numel() * buf.element_size()), "set_workspace")
+        self._workspace = buf
+
     def stability_bound(self, psi, stream=None) -> float:
         return nlse2shoc_stability_bound(self._h, self._check(psi), stream)
 

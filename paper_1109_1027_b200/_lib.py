@@ -70,6 +70,9 @@ def lib():
             "nlse2shoc_rk4": [H, ctypes.c_void_p, ctypes.c_double, ctypes.c_int64, ctypes.c_void_p],
             "nlse2shoc_stability_bound": [H, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_void_p],
             "nlse2shoc_check_finite": [H, ctypes.c_void_p, ctypes.c_void_p],
+            "nlse2shoc_set_workspace": [H, ctypes.c_void_p, ctypes.c_size_t],
+            "nlse2shoc_padded_layout": [H, i643, i643],
+            "nlse2shoc_rk4_padded": [H, ctypes.c_void_p, ctypes.c_double, ctypes.c_int64, ctypes.c_void_p],
         }
         for name, args in sig.items():
             if os.environ.get("NLSE_LIB") and not hasattr(L, name):
@@ -79,6 +82,9 @@ def lib():
             fn.restype = ctypes.c_int
         L.nlse2shoc_workspace_bytes.argtypes = [H]
         L.nlse2shoc_workspace_bytes.restype = ctypes.c_size_t
+        if hasattr(L, "nlse2shoc_stage_workspace_bytes"):
+            L.nlse2shoc_stage_workspace_bytes.argtypes = [H]
+            L.nlse2shoc_stage_workspace_bytes.restype = ctypes.c_size_t
         if hasattr(L, "nlse2shoc_exchange_timeouts"):
             L.nlse2shoc_exchange_timeouts.argtypes = [H]
             L.nlse2shoc_exchange_timeouts.restype = ctypes.c_int64
@@ -161,4 +167,5 @@ EXPORTS = [
     "nlse2shoc_rk4", "nlse2shoc_stability_bound", "nlse2shoc_check_finite", "nlse2shoc_last_launch_count",
     "nlse2shoc_strerror", "nlse2shoc_last_error", "nlse2shoc_version", "nlse2shoc_destroy",
     "nlse2shoc_set_allocator", "nlse2shoc_checked_violations",
+    "nlse2shoc_stage_workspace_bytes", "nlse2shoc_set_workspace", "nlse2shoc_padded_layout", "nlse2shoc_rk4_padded",
 ]

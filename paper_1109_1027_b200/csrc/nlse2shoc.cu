@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -148,6 +149,7 @@ struct nlse2shoc_s {
   std::vector<nlse2shoc_s *> slabs;
   bool loop_member = false;
   void *Lw = nullptr;  // pitched staging for the Laplacian output (odd-N_x complex64 only)
+  bool ws_external = false;  // T_A, T_B, acc live in the caller's workspace (nlse2shoc_set_workspace)
 #ifdef NLSE_WITH_NCCL
   ncclComm_t comm = nullptr;
 #endif
@@ -603,8 +605,10 @@ static nlse2shoc_status launch_two(int, int stage, const cplx<R> *in, const cplx
 //   1: acc = Psi + k/6 K1,  T_A = Psi + k/2 K1        3: acc += k/3 K3,  T_A = Psi + k K3
 //   2: acc += k/3 K2,       T_B = Psi + k/2 K2        4: Psi = acc + k/6 K4
 // s = 5 is the Laplacian (Psi -> L).
-// Write-light combine: the default of 2D/3D handles (variant 0) and variant 5.
-static bool write_light(const nlse2shoc_t H) { return H->variant == 0 || H->variant == 5; }
+// Carried-sum combine (DESIGN.md §5, 12 transfers): the default (variant 0) and variant 7.
+// Write-light combine (13 transfers): variant 5 (the default until r2's carried sum).
+static bool carried(const nlse2shoc_t H) { return H->variant == 0 || H->variant == 7; }
+static bool write_light(const nlse2shoc_t H) { return H->variant == 5; }
 
 // role of stage s's stencil input in the halo arena: 0 Psi, 1 T_A, 2 T_B, 3 acc
 static int input_role(const nlse2shoc_t H, int s) {
@@ -672,6 +676,30 @@ static nlse2shoc_status launch_stage(nlse2shoc_t H, Field &psi, int s, double dt
           *pB = reinterpret_cast<cplx<R> *>(H->TB.ptr), *pAcc = reinterpret_cast<cplx<R> *>(H->acc.ptr);
   // reconstructed-accumulator form (13 transfers per point-step): variant 6
   const bool recon = H->variant == 6;
+  if (carried(H)) {
+    // carried-sum form (12 transfers per point-step): stage 2 also stores
+    // Q = 3 acc - Psi; stage 3 writes T_C over T_A; stage 4 forms (Q + T_C + k/2 K4) / 3
+    switch (s) {
+      case 1:
+        P.cb = R(dt / 2.0); P.out_T = pA;
+        if constexpr (DIMS >= 2) return launch_stream<DIMS, R, M_S1R>(H, in, &psi.tm_pt, &H->acc.tm_pt, P, st);
+        else return launch_line<R, M_S1R>(H, in.ptr, psi.ptr, H->acc.ptr, P, st);
+      case 2:
+        P.ca = R(dt); P.cb = R(dt / 2.0); P.out_T = pB; P.out_acc = pAcc;
+        if constexpr (DIMS >= 2) return launch_stream<DIMS, R, M_S2Y>(H, in, &psi.tm_pt, &H->acc.tm_pt, P, st);
+        else return launch_line<R, M_S2Y>(H, in.ptr, psi.ptr, H->acc.ptr, P, st);
+      case 3:
+        P.cb = R(dt); P.out_T = pA;  // T_C
+        if constexpr (DIMS >= 2) return launch_stream<DIMS, R, M_S3R>(H, in, &psi.tm_pt, &H->acc.tm_pt, P, st);
+        else return launch_line<R, M_S3R>(H, in.ptr, psi.ptr, H->acc.ptr, P, st);
+      case 4:
+        P.cb = R(dt / 2.0); P.out_T = pPsi;  // k/2 K4 joins the numerator of the division by 3
+        if constexpr (DIMS >= 2) return launch_stream<DIMS, R, M_S4Y>(H, in, &psi.tm_pt, &H->acc.tm_pt, P, st);
+        else return launch_line<R, M_S4Y>(H, in.ptr, psi.ptr, H->acc.ptr, P, st);
+      default:
+        break;
+    }
+  }
   if (write_light(H)) {  // write-light form: T_A, T_B, T_C; acc never stored
     switch (s) {
       case 1:
@@ -734,7 +762,20 @@ static nlse2shoc_status launch_stage(nlse2shoc_t H, Field &psi, int s, double dt
   }
 }
 
+// NVTX ranges (per call, per stage, per halo exchange) for nsys / ncu --nvtx range
+// filters; the NVTX v3 calls are no-ops unless a tool is attached.  Inside a CUDA-graph
+// capture they mark the enqueue of the captured step, not its replays.
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
+
 static nlse2shoc_status stage(nlse2shoc_t H, Field &psi, int s, double dt, void *L, cudaStream_t st) {
+  static const char *const names[] = {"", "nlse2shoc stage 1", "nlse2shoc stage 2", "nlse2shoc stage 3",
+                                      "nlse2shoc stage 4", "nlse2shoc laplacian stage"};
+  NvtxRange nvtx_r(names[s >= 1 && s <= 5 ? s : 0]);
   const bool f32 = H->dtype == NLSE2SHOC_C64;
   switch (H->dims) {
     case 1: return f32 ? launch_stage<1, float>(H, psi, s, dt, L, st) : launch_stage<1, double>(H, psi, s, dt, L, st);
@@ -753,6 +794,7 @@ struct View {
 // Halo exchange of stage s's stencil input (2 planes per side): NCCL for a real shard,
 // device-to-device copies between the virtual slabs of a loopback handle.
 static nlse2shoc_status exchange(View &v, int s, cudaStream_t st) {
+  NvtxRange nvtx_r("nlse2shoc halo exchange");
   const size_t P = v.hs.size();
   if (P == 1) return halo_exchange(v.hs[0], stage_input(v.hs[0], v.psis[0], s), st);
   for (size_t i = 0; i < P; ++i) {
@@ -806,7 +848,7 @@ static bool resident_ok(nlse2shoc_t H) {
 static bool overlap_ok(const View &v) {
   bool multi = v.hs.size() > 1;
   for (nlse2shoc_t H : v.hs) {
-    if (!H->opt_overlap || H->dims < 2 || (H->variant != 0 && H->variant != 2 && H->variant != 5 && H->variant != 6) || H->nz < 8)
+    if (!H->opt_overlap || H->dims < 2 || (H->variant != 0 && H->variant != 2 && H->variant != 5 && H->variant != 6 && H->variant != 7) || H->nz < 8)
       return false;
     multi = multi || (H->sharded && H->nranks > 1);
   }
@@ -948,7 +990,7 @@ static nlse2shoc_status run_rk4_graph(View &v, double dt, int64_t nsteps, cudaSt
 static bool fused_ok(const View &v) {
   for (nlse2shoc_t H : v.hs)
     if (!H->peers || !H->opt_fused || H->dims < 2 ||
-        (H->variant != 0 && H->variant != 2 && H->variant != 5 && H->variant != 6))
+        (H->variant != 0 && H->variant != 2 && H->variant != 5 && H->variant != 6 && H->variant != 7))
       return false;
   return true;
 }
@@ -1258,9 +1300,10 @@ static nlse2shoc_status wrap_psi(nlse2shoc_t S, void *base, Field &w) {
 
 // Build the view of a call on psi (caller layout).  *work receives the pitched base the
 // kernels use (== psi on the zero-copy path).
-static nlse2shoc_status make_view(nlse2shoc_t H, void *psi, View &v, void **work, cudaStream_t st) {
+static nlse2shoc_status make_view(nlse2shoc_t H, void *psi, View &v, void **work, cudaStream_t st,
+                                  bool padded = false) {
   void *base = psi;
-  if (H->pitch != H->nx) {
+  if (H->pitch != H->nx && !padded) {
     base = H->psiw.ptr;
     CUDA_TRY(cudaMemcpy2DAsync(base, H->pitch * H->S, psi, H->nx * H->S, H->nx * H->S, H->ny * H->nz,
                                cudaMemcpyDeviceToDevice, st));
@@ -1440,10 +1483,10 @@ size_t nlse2shoc_workspace_bytes(nlse2shoc_t H) {
 nlse2shoc_status nlse2shoc_set_variant(nlse2shoc_t H, int variant) {
   if (!H) return fail(NLSE2SHOC_EINVAL, "NULL handle");
   DeviceGuard dg(H->device);
-  if (variant < 0 || variant > 6)
+  if (variant < 0 || variant > 7)
     return fail(NLSE2SHOC_EINVAL, "variant must be 0 (fused default), 1 (two-kernel), 2 (fused, 16-transfer "
                                   "accumulator), 3 (two-kernel, multi-storage), 4 (stage pairs), 5 (fused, "
-                                  "write-light) or 6 (fused, reconstructed accumulator)");
+                                  "write-light), 6 (fused, reconstructed accumulator) or 7 (fused, carried sum)");
   if (variant == 4 && (H->dims < 2 || !H->slabs.empty() || H->sharded))
     return fail(NLSE2SHOC_EUNSUPPORTED, "the stage-pair variant needs a single-slab 2D/3D handle");
   if ((variant == 1 || variant == 3) && H->scheme != NLSE2SHOC_SCHEME_2SHOC)
@@ -1531,6 +1574,7 @@ nlse2shoc_status nlse2shoc_set_scheme(nlse2shoc_t H, int scheme) {
 }
 
 nlse2shoc_status nlse2shoc_laplacian(nlse2shoc_t H, const void *psi, void *L, void *stream) {
+  NvtxRange nvtx_r("nlse2shoc_laplacian");
   if (!H) return fail(NLSE2SHOC_EINVAL, "NULL handle");
   DeviceGuard dg(H->device);
   TRY(check_ptr(psi, "psi"));
@@ -1553,10 +1597,12 @@ nlse2shoc_status nlse2shoc_laplacian(nlse2shoc_t H, const void *psi, void *L, vo
   return unstage(H, L, dst, st);
 }
 
-nlse2shoc_status nlse2shoc_rk4(nlse2shoc_t H, void *psi, double dt, int64_t nsteps, void *stream) {
+static nlse2shoc_status rk4_entry(nlse2shoc_t H, void *psi, double dt, int64_t nsteps, void *stream, bool padded) {
+  NvtxRange nvtx_r("nlse2shoc_rk4");
   if (!H) return fail(NLSE2SHOC_EINVAL, "NULL handle");
   DeviceGuard dg(H->device);
   TRY(check_ptr(psi, "psi"));
+  if (padded && (reinterpret_cast<uintptr_t>(psi) & 15)) return fail(NLSE2SHOC_EINVAL, "padded psi must be 16-byte aligned");
   if (!finite_pos(dt)) return fail(NLSE2SHOC_EINVAL, "dt must be finite and > 0");
   if (nsteps < 0) return fail(NLSE2SHOC_EINVAL, "nsteps must be >= 0");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -1564,12 +1610,65 @@ nlse2shoc_status nlse2shoc_rk4(nlse2shoc_t H, void *psi, double dt, int64_t nste
   if (nsteps == 0) return NLSE2SHOC_OK;
   View v;
   void *work = nullptr;
-  TRY(make_view(H, psi, v, &work, st));
+  TRY(make_view(H, psi, v, &work, st, padded));
   TRY(run_rk4(v, dt, nsteps, st));
   return unstage(H, psi, work, st);
 }
 
+nlse2shoc_status nlse2shoc_rk4(nlse2shoc_t H, void *psi, double dt, int64_t nsteps, void *stream) {
+  return rk4_entry(H, psi, dt, nsteps, stream, false);
+}
+
+nlse2shoc_status nlse2shoc_rk4_padded(nlse2shoc_t H, void *psi, double dt, int64_t nsteps, void *stream) {
+  return rk4_entry(H, psi, dt, nsteps, stream, true);
+}
+
+nlse2shoc_status nlse2shoc_padded_layout(nlse2shoc_t H, int64_t pitch[3], int64_t offset[3]) {
+  if (!H || !pitch || !offset) return fail(NLSE2SHOC_EINVAL, "NULL argument");
+  pitch[0] = H->pitch;        // elements per x-row
+  pitch[1] = H->plane;        // elements per plane (pitch * N_y; 2D: per row)
+  pitch[2] = H->local_elems;  // elements of the local field
+  offset[0] = offset[1] = offset[2] = 0;  // no ghost layers in memory: ghosts are formed on chip
+  return NLSE2SHOC_OK;
+}
+
+size_t nlse2shoc_stage_workspace_bytes(nlse2shoc_t H) {
+  if (!H) return 0;
+  const size_t f = ((size_t(H->local_elems) * H->S + 255) / 256) * 256;
+  return 3 * f;
+}
+
+nlse2shoc_status nlse2shoc_set_workspace(nlse2shoc_t H, void *dev, size_t bytes) {
+  if (!H) return fail(NLSE2SHOC_EINVAL, "NULL handle");
+  DeviceGuard dg(H->device);
+  if (!H->slabs.empty() || H->loop_member)
+    return fail(NLSE2SHOC_EUNSUPPORTED, "set_workspace: loopback handles own their slabs' workspaces");
+  if (!dev || (reinterpret_cast<uintptr_t>(dev) & 255)) return fail(NLSE2SHOC_EINVAL, "workspace must be a 256-byte aligned device pointer");
+  if (bytes < nlse2shoc_stage_workspace_bytes(H)) return fail(NLSE2SHOC_EINVAL, "workspace smaller than nlse2shoc_stage_workspace_bytes");
+  cudaPointerAttributes pa;
+  if (cudaPointerGetAttributes(&pa, dev) != cudaSuccess || pa.type != cudaMemoryTypeDevice || pa.device != H->device) {
+    cudaGetLastError();
+    return fail(NLSE2SHOC_EINVAL, "workspace is not device memory of the handle's device");
+  }
+  CUDA_TRY(cudaDeviceSynchronize());  // nothing in flight may still use the old fields
+  graph_drop(H);
+  const size_t f = nlse2shoc_stage_workspace_bytes(H) / 3, own = size_t(H->local_elems) * H->S;
+  int i = 0;
+  for (Field *fl : {&H->TA, &H->TB, &H->acc}) {
+    if (!H->ws_external && fl->ptr) {
+      CUDA_TRY(dev_free(H, fl->ptr));
+      H->bytes -= own;
+    }
+    fl->ptr = reinterpret_cast<char *>(dev) + size_t(i++) * f;
+    TRY(encode_maps(H, *fl));
+  }
+  H->ws_external = true;
+  ++H->gen;
+  return NLSE2SHOC_OK;
+}
+
 nlse2shoc_status nlse2shoc_stability_bound(nlse2shoc_t H, const void *psi, double *kmax, void *stream) {
+  NvtxRange nvtx_r("nlse2shoc_stability_bound");
   if (!H || !kmax) return fail(NLSE2SHOC_EINVAL, "NULL argument");
   DeviceGuard dg(H->device);
   TRY(check_ptr(psi, "psi"));
@@ -1673,8 +1772,10 @@ void nlse2shoc_destroy(nlse2shoc_t H) {
   cudaDeviceSynchronize();
   for (nlse2shoc_t S : H->slabs) nlse2shoc_destroy(S);
   if (H->Lw) dev_free(H, H->Lw);
-  for (Field *f : {&H->TA, &H->TB, &H->acc, &H->psiw, &H->D})
+  for (Field *f : {&H->TA, &H->TB, &H->acc, &H->psiw, &H->D}) {
+    if (H->ws_external && (f == &H->TA || f == &H->TB || f == &H->acc)) continue;  // the caller's memory
     if (f->ptr) dev_free(H, f->ptr);
+  }
   if (H->ipc_lo) cudaIpcCloseMemHandle(H->ipc_lo);
   if (H->ipc_hi) cudaIpcCloseMemHandle(H->ipc_hi);
   if (H->arena) cudaFree(H->arena);

@@ -95,6 +95,12 @@ __global__ void __launch_bounds__(256) stage_line_kernel(const cplx<R> *__restri
       const CT ps = psi[i];
       const CT dsum = axpy(acc[i] - ps, R(2), t3[i] - ps) + (c - ps);
       P.out_T[i] = iaxpy(axpy(ps, R(1.0 / 3.0), dsum), P.cb, t);
+    } else if (MODE == M_S2Y) {  // carried sum (variant 7): Q = 3 acc - Psi
+      const CT ps = psi[i];
+      P.out_acc[i] = iaxpy(axpy(c - ps, R(2), ps), P.ca, t);
+      P.out_T[i] = iaxpy(ps, P.cb, t);
+    } else if (MODE == M_S4Y) {  // Psi' = (Q + T_C + k/2 K4) / 3; a Dirichlet end keeps T_C = Psi_b
+      P.out_T[i] = ((i == 0 || i == n - 1) && P.bc == 0) ? c : carry3(acc[i], c, P.cb, t);
     } else if (MODE == M_S2 || MODE == M_S3) {
       P.out_acc[i] = iaxpy(acc[i], P.ca, t);
       P.out_T[i] = iaxpy(psi[i], P.cb, t);
@@ -155,6 +161,12 @@ __global__ void __launch_bounds__(256) line_tile_kernel(const cplx<R> *__restric
       const CT ps = psi[i];
       const CT dsum = axpy(acc[i] - ps, R(2), t3[i] - ps) + (c - ps);
       P.out_T[i] = iaxpy(axpy(ps, R(1.0 / 3.0), dsum), P.cb, t);
+    } else if (MODE == M_S2Y) {  // carried sum (variant 7): Q = 3 acc - Psi
+      const CT ps = psi[i];
+      P.out_acc[i] = iaxpy(axpy(c - ps, R(2), ps), P.ca, t);
+      P.out_T[i] = iaxpy(ps, P.cb, t);
+    } else if (MODE == M_S4Y) {  // Psi' = (Q + T_C + k/2 K4) / 3; a Dirichlet end keeps T_C = Psi_b
+      P.out_T[i] = ((i == 0 || i == n - 1) && P.bc == 0) ? c : carry3(acc[i], c, P.cb, t);
     } else if (MODE == M_S2 || MODE == M_S3) {
       P.out_acc[i] = iaxpy(acc[i], P.ca, t);
       P.out_T[i] = iaxpy(psi[i], P.cb, t);
@@ -180,7 +192,7 @@ template <typename R> struct LineStream {
 };
 template <typename R, int MODE> __host__ __device__ constexpr int line_npa() {
   return MODE == M_S4X ? 3 : ((MODE == M_S4R || MODE == M_S2 || MODE == M_S3 || MODE == M_S4) ? 2 :
-                              ((MODE == M_S2R || MODE == M_S3R) ? 1 : 0));
+                              ((MODE == M_S2R || MODE == M_S3R || MODE == M_S2Y || MODE == M_S4Y) ? 1 : 0));
 }
 template <typename R, int MODE> __host__ __device__ constexpr size_t line_stream_smem() {
   using LS = LineStream<R>;
@@ -205,7 +217,7 @@ __global__ void __launch_bounds__(256, LineStream<R>::MINB) line_stream_kernel(c
     fence_mbar_init();
   }
   __syncthreads();
-  const CT *pstream[3] = {psi, acc, t3};
+  const CT *pstream[3] = {MODE == M_S4Y ? acc : psi, acc, t3};  // M_S4Y streams the carried sum alone
   auto seg_of = [&](int j) { const int sg = blockIdx.x + j * gridDim.x; return P.rev ? nseg - 1 - sg : sg; };
   auto interior = [&](int sg) { return int64_t(sg) * SEG - 4 >= 0 && int64_t(sg + 1) * SEG + 4 <= n; };
   auto issue = [&](int j) {  // thread 0: prefetch segment j into ring stage j % NS
@@ -275,6 +287,11 @@ __global__ void __launch_bounds__(256, LineStream<R>::MINB) line_stream_kernel(c
       } else if (MODE == M_S4X) {
         const CT dsum = axpy(a1 - ps, R(2), a2 - ps) + (c - ps);
         P.out_T[i] = iaxpy(axpy(ps, R(1.0 / 3.0), dsum), P.cb, t);
+      } else if (MODE == M_S2Y) {
+        P.out_acc[i] = iaxpy(axpy(c - ps, R(2), ps), P.ca, t);
+        P.out_T[i] = iaxpy(ps, P.cb, t);
+      } else if (MODE == M_S4Y) {  // the one pointwise stream is the carried sum Q
+        P.out_T[i] = ((i == 0 || i == n - 1) && P.bc == 0) ? c : carry3(ps, c, P.cb, t);
       } else if (MODE == M_S1) {
         P.out_acc[i] = iaxpy(c, P.ca, t);
         P.out_T[i] = iaxpy(c, P.cb, t);

@@ -35,7 +35,15 @@ namespace nlse {
 // Psi' = acc + (T_A - Psi)/3 + k/6 K4 ((T_A - Psi)/3 = k/3 K3): 13 transfers in all.
 // M_S4X (variant 5): stage 4 of the write-light form: Psi' = Psi + ((T_A - Psi) + 2 (T_B - Psi) +
 // (T_C - Psi)) / 3 + k/6 K4 from the stencil input T_C and pointwise Psi, T_A, T_B.
-enum Mode { M_S1 = 1, M_S2 = 2, M_S3 = 3, M_S4 = 4, M_LAP = 5, M_S1R = 6, M_S2R = 7, M_S3R = 8, M_S4R = 9, M_S4X = 10 };
+// M_S2Y / M_S4Y (variant 7, carried sum: 12 transfers): stage 2 also stores
+// Q = 3 acc - Psi = [2 Psi + (T_A - Psi)] + k K2 (acc = Psi + k/6 K1 + k/3 K2), and stage 4
+// forms Psi' = (Q + T_C + k/2 K4) / 3 from its stencil input T_C = Psi + k K3 and Q alone:
+// the sum Q + T_C is carried exactly (s + e), divided by 3 with a correctly rounded quotient
+// (q = fl(s w), r = s - 3 q exactly, Psi' = fl(q + w (r + e + k/2 K4))), so a stationary field
+// and Dirichlet boundary values are reproduced to the bit and no rounding error is
+// systematic (carry3 below; a carried acc - fl(1/3) Psi drifts linearly with the step count).
+enum Mode { M_S1 = 1, M_S2 = 2, M_S3 = 3, M_S4 = 4, M_LAP = 5, M_S1R = 6, M_S2R = 7, M_S3R = 8, M_S4R = 9, M_S4X = 10,
+            M_S2Y = 11, M_S4Y = 12 };
 
 // Tile configuration per (dims, precision).  W = smem row width in complex elements
 // (tile + 2+2 halo, rounded so that it splits into NBOX equal TMA boxes); every TMA
@@ -161,15 +169,16 @@ template <int DIMS, typename R> struct Layout {
   static_assert(C::NBOXP == 1 || (BWP * 8) % 128 == 0, "P sub-boxes 128-byte aligned");
   static_assert((C::TX / C::PPX) * (C::TY / C::RPW) == C::NCW * 32, "thread map");
   template <int MODE> __host__ __device__ static constexpr bool needs_psi() {
-    return MODE == M_S2 || MODE == M_S3 || MODE == M_S2R || MODE == M_S3R || MODE == M_S4R || MODE == M_S4X;
+    return MODE == M_S2 || MODE == M_S3 || MODE == M_S2R || MODE == M_S3R || MODE == M_S4R || MODE == M_S4X ||
+           MODE == M_S2Y;
   }
   // third pointwise tile (M_S4X: T_B; its second tile, in the acc position, is T_A)
   template <int MODE> __host__ __device__ static constexpr bool needs_t3() { return MODE == M_S4X; }
   template <int MODE> __host__ __device__ static constexpr bool writes_acc() {
-    return MODE == M_S1 || MODE == M_S2 || MODE == M_S3 || MODE == M_S2R;
+    return MODE == M_S1 || MODE == M_S2 || MODE == M_S3 || MODE == M_S2R || MODE == M_S2Y;
   }
   template <int MODE> __host__ __device__ static constexpr bool needs_acc() {
-    return MODE == M_S2 || MODE == M_S3 || MODE == M_S4 || MODE == M_S4R || MODE == M_S4X;
+    return MODE == M_S2 || MODE == M_S3 || MODE == M_S4 || MODE == M_S4R || MODE == M_S4X || MODE == M_S4Y;
   }
   template <int MODE> __host__ __device__ static constexpr int pa_tiles() {
     return (needs_psi<MODE>() ? 1 : 0) + (needs_acc<MODE>() ? 1 : 0) + (needs_t3<MODE>() ? 1 : 0);
@@ -235,6 +244,20 @@ __device__ __forceinline__ cplx<R> lap_wide(cplx<R> c, R w16x, R w1x, R w16y, R 
   L = lap5(L, c2, w16z, w1z, zm1, zp1, zm2, zp2);
   if (DIMS == 3) L = lap5(L, c2, w16y, w1y, ym1, yp1, ym2, yp2);
   return L;
+}
+
+// Stage 4 of the carried-sum form (M_S4Y): (Q + T_C + kh tF i) / 3 with Q = 3 acc - Psi, kh = k/2.
+// s + e = Q + T_C exactly (|Q| ~ 2 |T_C|: Dekker's fast two-sum), q = fl(s w) with w = fl(1/3),
+// r = s - 3 q exactly (one FMA), result = fl(q + w (r + e + kh i tF)): the quotient is correctly
+// rounded (its candidates lie thirds of an ulp apart, never at a tie), the RK4 increment
+// k/6 K4 rides in the remainder, and the whole stage has a single rounding of size ulp(Psi).
+template <typename R> __device__ __forceinline__ cplx<R> carry3(cplx<R> Q, cplx<R> TC, R kh, cplx<R> tF) {
+  const cplx<R> s = Q + TC;
+  const cplx<R> e = TC - (s - Q);
+  const cplx<R> q = R(1.0 / 3.0) * s;
+  cplx<R> r = axpy(s, R(-3), q);
+  r = iaxpy(r + e, kh, tF);
+  return axpy(q, R(1.0 / 3.0), r);
 }
 
 // Shared-memory 128-bit helpers: CPV complex values per 16-byte vector.
@@ -697,12 +720,13 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
           else V = (vxr[q] + vyr[r]) + vzk;
           const R N = fma(ps_, norm2(c), -V);
           CT tF;  // F = i tF
+          bool bnd = false;
           if (fast) {
             valid[q] = true;
             tF = axpy(N * c, pa_, L);  // a L + N c
           } else {
             valid[q] = gx < nx && gy < ny;
-            const bool bnd = gx == 0 || gx == nx - 1 || (DIMS == 3 && (gy == 0 || gy == ny - 1)) || !zint;
+            bnd = gx == 0 || gx == nx - 1 || (DIMS == 3 && (gy == 0 || gy == ny - 1)) || !zint;
             if (!bnd) {
               tF = axpy(N * c, pa_, L);
             } else {
@@ -728,6 +752,12 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
             // acc = (T_A + 2 T_B) / 3 in exact arithmetic; the differences keep it to O(k)
             const CT dsum = axpy(acv[q] - psv[q], R(2), t3v[q] - psv[q]) + (c - psv[q]);
             oT[q] = iaxpy(axpy(psv[q], R(1.0 / 3.0), dsum), cb, tF);
+          } else if (MODE == M_S2Y) {
+            oA[q] = iaxpy(axpy(c - psv[q], R(2), psv[q]), ca, tF);  // Q = (2 Psi + (T_A - Psi)) + k K2
+            oT[q] = iaxpy(psv[q], cb, tF);
+          } else if (MODE == M_S4Y) {
+            // Dirichlet boundary points: T_C = Psi to the bit (F_b = 0), and Psi_b is kept
+            oT[q] = (bnd && P.bc == 0) ? c : carry3(acv[q], c, cb, tF);
           } else if (MODE == M_S2 || MODE == M_S3) {
             oA[q] = iaxpy(acv[q], ca, tF);
             oT[q] = iaxpy(psv[q], cb, tF);
@@ -897,8 +927,9 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
           else V = (vxr[q] + vyr[r]) + vzk;
           const R N = fma(ps_, norm2(c), -V);
           CT tF = axpy(N * c, pa_, L);  // F = i (a L + N c)
-          if (XF && (x0 + lx0 + q == 0 || x0 + lx0 + q == nx - 1 || y0 + ly0 + r == 0 ||
-                     y0 + ly0 + r == ny - 1)) {  // boundary column / row (face rule)
+          const bool bnd = XF && (x0 + lx0 + q == 0 || x0 + lx0 + q == nx - 1 || y0 + ly0 + r == 0 ||
+                                  y0 + ly0 + r == ny - 1);
+          if (bnd) {  // boundary column / row (face rule)
             L = lambda_b(P, c, V);
             tF = P.bc == 0 ? zero : N * c;
           }
@@ -920,6 +951,11 @@ __global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
             // acc = (T_A + 2 T_B) / 3 in exact arithmetic; the differences keep it to O(k)
             const CT dsum = axpy(acv[q] - psv[q], R(2), t3v[q] - psv[q]) + (c - psv[q]);
             oT[q] = iaxpy(axpy(psv[q], R(1.0 / 3.0), dsum), cb, tF);
+          } else if (MODE == M_S2Y) {
+            oA[q] = iaxpy(axpy(c - psv[q], R(2), psv[q]), ca, tF);  // Q = (2 Psi + (T_A - Psi)) + k K2
+            oT[q] = iaxpy(psv[q], cb, tF);
+          } else if (MODE == M_S4Y) {
+            oT[q] = (bnd && P.bc == 0) ? c : carry3(acv[q], c, cb, tF);
           } else if (MODE == M_S2 || MODE == M_S3) {
             oA[q] = iaxpy(acv[q], ca, tF);
             oT[q] = iaxpy(psv[q], cb, tF);

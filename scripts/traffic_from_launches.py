@@ -22,6 +22,6 @@ tot = sum(v["dram__bytes_read.sum"] + v["dram__bytes_write.sum"] for v in launch
 bps = tot / len(launches) / npts
 res = {"workload": wl, "source": f"{path} (ncu dram__bytes_read/write.sum, {len(launches)} stage launches)",
        "dram_bytes_per_point_stage": round(bps, 4), "dram_bytes_per_point_step": round(4 * bps, 2),
-       "algorithmic_bytes_per_point_step_16S": 128, "moved_by_design_13S": 104}
+       "algorithmic_bytes_per_point_step_16S": 128, "moved_by_design_12S": 96}
 json.dump(res, open(out, "w"), indent=1)
 print(json.dumps(res))

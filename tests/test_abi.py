@@ -57,6 +57,12 @@ def test_create_rejects_bad_arguments_without_touching_the_gpu():
     n2 = (ctypes.c_int64 * 3)(8, 3, 1)
     assert L.nlse2shoc_create(ctypes.byref(H), 1, n2, h, 1.0, 1.0, None, 0, 0) == _lib.EINVAL  # unused axis != 1
     assert H.value is None
+    # the optional workspace / layout calls validate their handle before anything else
+    assert L.nlse2shoc_set_workspace(None, None, 0) == _lib.EINVAL
+    assert L.nlse2shoc_stage_workspace_bytes(None) == 0
+    p3 = (ctypes.c_int64 * 3)()
+    assert L.nlse2shoc_padded_layout(None, p3, p3) == _lib.EINVAL
+    assert L.nlse2shoc_rk4_padded(None, None, 1e-3, 1, None) == _lib.EINVAL
 
 
 def test_product_package_never_imports_oracle():

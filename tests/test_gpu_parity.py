@@ -57,7 +57,7 @@ def test_laplacian_parity(dims, n, dtype, bc, V, variant):
     H.compare(L.cpu().numpy(), Lo, tol, "")
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7])
 @pytest.mark.parametrize("dims,n,dtype,bc,V", CASES[::2])
 def test_rk4_parity_10_steps(dims, n, dtype, bc, V, variant):
     if variant == 4 and dims == 1:
@@ -122,11 +122,14 @@ def test_edge_cases_and_errors():
     S.check_finite(psi)
 
 
-def test_dirichlet_boundary_values_are_bit_exact():
-    """`dbc_ut`: Psi_t,b = 0, so boundary values never change, to the bit."""
-    w = _small(3, (37, 19, 9), "dirichlet", "c128", "harmonic")
-    S = H.gpu_solver(w, "c128")
-    psi = H.psi0_host(w, "c128")
+@pytest.mark.parametrize("variant,n,dtype", [(0, (37, 19, 9), "c128"), (5, (37, 19, 9), "c128"), (6, (37, 19, 9), "c64"),
+                                              (0, (131, 51, 12), "c64"), (0, (70, 67, 10), "c128")])
+def test_dirichlet_boundary_values_are_bit_exact(variant, n, dtype):
+    """`dbc_ut`: Psi_t,b = 0, so boundary values never change, to the bit (the default
+    carried-sum form returns T_C,b = Psi_b at boundary points; grids with face-lean tiles too)."""
+    w = _small(3, n, "dirichlet", dtype, "harmonic")
+    S = H.gpu_solver(w, dtype, variant)
+    psi = H.psi0_host(w, dtype)
     g = _dev(psi)
     S.rk4(g, 1e-4, 7)
     out = g.cpu().numpy()
@@ -135,7 +138,7 @@ def test_dirichlet_boundary_values_are_bit_exact():
     assert np.array_equal(out[m], psi[m])
 
 
-@pytest.mark.parametrize("variant", [0, 2, 4, 6])
+@pytest.mark.parametrize("variant", [0, 2, 4, 5, 6])
 @pytest.mark.parametrize("dims,n,dtype,bc,V", [c for c in CASES if c[0] > 1][1::3])
 def test_rk4_parity_isotropic(dims, n, dtype, bc, V, variant):
     """Equal spacing on every axis selects the kernels' summed-neighbour stencil form."""
@@ -155,7 +158,7 @@ def test_rk4_parity_isotropic(dims, n, dtype, bc, V, variant):
 @pytest.mark.parametrize("dims,n,aniso", [(1, (3000,), True), (2, (300, 70), False), (2, (300, 70), True),
                                           (3, (80, 40, 20), False), (3, (80, 40, 20), True)])
 @pytest.mark.parametrize("bc", ["dirichlet", "lapzero"])
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5])
 def test_constant_field_is_stationary_to_the_bit(dims, n, aniso, bc, variant):
     """s = 0, V = 0, Psi = const: the exact Laplacian is 0, so Psi_t = 0 and RK4 must return
     Psi unchanged.  The stencil is written with the centre inside each difference (lap5 /
@@ -257,11 +260,13 @@ def test_C2_full_500_steps(dtype):
     psi = H.psi0_host(w, dtype)
     P = H.oracle_problem(w)
     dt = 0.8 * oracle.kmax(P, psi.astype(np.complex128))
-    S = H.gpu_solver(w, dtype)
-    g = _dev(psi)
-    S.rk4(g, dt, w["steps"])
     ref = oracle.rk4(P, psi.astype(np.complex128), dt, w["steps"])
-    H.compare(g.cpu().numpy(), ref, H.TOL[dtype], f"C2 {dtype} 500 steps, full grid")
+    for variant in (0, 5):  # the default (carried sum, 12 transfers) and the write-light form (13)
+        S = H.gpu_solver(w, dtype, variant)
+        g = _dev(psi)
+        S.rk4(g, dt, w["steps"])
+        H.compare(g.cpu().numpy(), ref, H.TOL[dtype], f"C2 {dtype} 500 steps, full grid, variant {variant}")
+        S.close()
 
 
 def _crop_parity(w, dtype, nsteps, targets, name, variant=0):
@@ -356,7 +361,8 @@ def _core_box_work(w, lo, cnt):
     return wc
 
 
-@pytest.mark.parametrize("dtype,variant", [("c64", 0), ("c64", 2), ("c64", 6), ("c128", 0), ("c128", 6)])
+@pytest.mark.parametrize("dtype,variant", [("c64", 0), ("c64", 2), ("c64", 5), ("c64", 6), ("c128", 0), ("c128", 5),
+                                           ("c128", 6)])
 def test_C4_core_box_full_step_count(dtype, variant):
     """C4 at its stated step count (100) on a 96^3 box around the ring core with C4's own
     spacing (SURVEY A7 analogue): the whole-field parity the north star states, for the
@@ -428,7 +434,7 @@ def test_fig1_on_gpu():
         assert abs(metrics.order(E[2 * h2][0], E[h2][0], 2 * h2, h2) - o) < 5e-3
 
 
-@pytest.mark.parametrize("variant", [0, 2, 6])
+@pytest.mark.parametrize("variant", [0, 2, 5, 6])
 @pytest.mark.parametrize("bc,V,dtype", [("dirichlet", "harmonic", "c128"), ("lapzero", "array", "c128"),
                                         ("dirichlet", "none", "c64"), ("lapzero", "harmonic", "c128")])
 def test_1d_stream_kernel_parity(bc, V, dtype, variant):
@@ -471,7 +477,7 @@ def _ragged_cases():
     return out
 
 
-@pytest.mark.parametrize("variant", [0, 2, 6])
+@pytest.mark.parametrize("variant", [0, 2, 5, 6])
 @pytest.mark.parametrize("dtype,n,bc", _ragged_cases())
 def test_lean_steps_bit_identical_to_general_step(dtype, n, bc, variant):
     """The lean plane steps (interior tiles, and 3D tiles touching an x/y face with the ghost
@@ -585,3 +591,96 @@ def test_cached_step_graph(shard):
     assert torch.equal(c, d)
     assert not torch.equal(a, c)
     S.close()
+
+
+@pytest.mark.parametrize("dims,n,dtype", [(3, (70, 30, 20), "c64"), (2, (1100, 37), "c128"), (1, (40003,), "c64")])
+def test_caller_owned_workspace(dims, n, dtype):
+    """nlse2shoc_set_workspace: the three stage fields in a torch tensor give the
+    same bits as the library's own allocation, the handle's own byte count drops by them, and
+    bad workspaces are refused."""
+    import paper_1109_1027_b200 as nl
+
+    w = _small(dims, n, "dirichlet", dtype, "harmonic")
+    psi = H.psi0_host(w, dtype)
+    S = nl.solver_from_work(w, dtype)
+    a = _dev(psi)
+    dt = 0.5 * S.stability_bound(a)
+    S.rk4(a, dt, 6)
+    need, before = S.stage_workspace_bytes, S.workspace_bytes
+    assert need >= 3 * psi.nbytes and need % 256 == 0
+    ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+    S.set_workspace(ws)
+    assert before - S.workspace_bytes == 3 * psi.nbytes
+    b = _dev(psi)
+    S.rk4(b, dt, 6)
+    assert torch.isfinite(torch.view_as_real(a)).all() and torch.equal(a, b)
+    L0, L1 = S.laplacian(a), S.laplacian(b)
+    assert torch.equal(L0, L1)
+    with pytest.raises(nl.NLSE2SHOCError):
+        S.set_workspace(torch.empty(need - 256, dtype=torch.uint8, device="cuda"))
+    with pytest.raises(nl.NLSE2SHOCError):
+        S.set_workspace(torch.empty(need + 256, dtype=torch.uint8, device="cuda")[8:])
+    ws2 = torch.empty(need, dtype=torch.uint8, device="cuda")  # a second workspace replaces the first
+    S.set_workspace(ws2)
+    c = _dev(psi)
+    S.rk4(c, dt, 6)
+    assert torch.equal(a, c)
+    S.close()
+    L = nl.solver_from_work(w, dtype, shard={"loopback": 2}) if dims > 1 else None
+    if L is not None:
+        with pytest.raises(nl.NLSE2SHOCError):
+            L.set_workspace(ws)
+        L.close()
+
+
+@pytest.mark.parametrize("dims,n", [(3, (71, 30, 20)), (2, (1101, 37)), (3, (70, 30, 20))])
+def test_padded_layout_zero_copy(dims, n):
+    """nlse2shoc_padded_layout / nlse2shoc_rk4_padded: complex64 with odd N_x is
+    staged through a pitched copy by rk4; a Psi already in the padded layout is used in place
+    and gives the same bits, its pad column untouched.  Even N_x: the layout is the dense one."""
+    import paper_1109_1027_b200 as nl
+
+    w = _small(dims, n, "lapzero", "c64", "harmonic")
+    psi = H.psi0_host(w, "c64")
+    S = nl.solver_from_work(w, "c64")
+    pitch, off = S.padded_layout
+    assert off == [0, 0, 0] and pitch[0] == n[0] + (n[0] & 1)
+    assert pitch[1] == pitch[0] * (n[1] if dims == 3 else 1) and pitch[2] == pitch[0] * int(np.prod(n[1:]))
+    a = _dev(psi)
+    S.rk4(a, 1e-4, 5)
+    p = torch.full(tuple(psi.shape[:-1]) + (pitch[0],), complex(7.0, -7.0), dtype=torch.complex64, device="cuda")
+    p[..., :n[0]] = _dev(psi)
+    S.rk4_padded(p, 1e-4, 5)
+    assert torch.equal(p[..., :n[0]], a)
+    if pitch[0] != n[0]:
+        assert torch.all(p[..., n[0]] == complex(7.0, -7.0))
+    with pytest.raises(ValueError):
+        S.rk4_padded(a if pitch[0] != n[0] else a[..., :-1], 1e-4, 1)
+    S.close()
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("dims,n", [(1, (3000,)), (1, (40003,)), (2, (300, 70)), (3, (80, 40, 20))])
+def test_carried_sum_keeps_any_constant_to_the_bit(dims, n, dtype):
+    """The default (carried-sum, 12-transfer) combine forms Psi' = (Q + T_C + k/2 K4) / 3 with
+    Q = 3 acc - Psi: its exact sum and correctly rounded division must return a stationary
+    field unchanged for any mantissa (a plain Q + fl(1/3) T_C does not), and variant 0 is
+    variant 7."""
+    w = _small(dims, n, "lapzero", dtype, "none", aniso=False)
+    w["s"] = 0.0
+    tdt = torch.complex64 if dtype == "c64" else torch.complex128
+    S = H.gpu_solver(w, dtype)
+    for val in (complex(1 / 3, 2 / 3), complex(1.9999999, -1.3333334), complex(5e-5, 123.456), complex(-0.7, 1e-30)):
+        g = torch.full(tuple(reversed(n)), val, dtype=tdt, device="cuda")
+        g0 = g.clone()
+        S.rk4(g, 0.5 * S.stability_bound(g), 20)
+        assert torch.equal(g, g0), val
+    w2 = _small(dims, n, "dirichlet", dtype, "harmonic")
+    psi = H.psi0_host(w2, dtype)
+    outs = []
+    for v in (0, 7):
+        S2 = H.gpu_solver(w2, dtype, v)
+        g = _dev(psi)
+        S2.rk4(g, 0.5 * S2.stability_bound(g), 5)
+        outs.append(g.cpu())
+    assert torch.isfinite(torch.view_as_real(outs[0])).all() and torch.equal(outs[0], outs[1])

@@ -40,7 +40,7 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 6])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 5, 6])
 @pytest.mark.parametrize("nslabs", [2, 3, 7])
 @pytest.mark.parametrize("dims,n,bc,dtype,V", CASES)
 def test_loopback_bitwise_equal(dims, n, bc, dtype, V, nslabs, variant):
@@ -127,7 +127,7 @@ def test_loopback_C4_seams_match_oracle():
         H.compare(gb, want, 1e-5, f"C4 loopback P=8 10 steps, seam box {tlo}+{tcnt}")
 
 
-@pytest.mark.parametrize("variant", [0, 2, 6])
+@pytest.mark.parametrize("variant", [0, 2, 5, 6])
 @pytest.mark.parametrize("nslabs", [2, 3, 8])
 def test_fused_exchange_bitwise_and_one_launch_per_stage(nslabs, variant):
     """Halo exchange fused into the stage kernels (loopback slabs are each other's peers): the
