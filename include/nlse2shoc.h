@@ -167,8 +167,8 @@ nlse2shoc_status nlse2shoc_padded_layout(nlse2shoc_t, int64_t pitch[3], int64_t 
 nlse2shoc_status nlse2shoc_rk4_padded(nlse2shoc_t, void *psi_padded, double dt, int64_t nsteps, void *stream);
 
 /* 0 = FUSED (default): one kernel per RK4 stage computes the whole 2SHOC Laplacian (both
- *     steps, D never stored), the RHS and the RK4 stage combine, 13 field transfers per
- *     point-step, in the write-light form (= variant 5).
+ *     steps, D never stored), the RHS and the RK4 stage combine, 12 field transfers per
+ *     point-step, in the carried-sum form (= variant 7).
  * 5 = FUSED_WRITE_LIGHT: stages 1-3 store only T_A = Psi + k/2 K1, T_B = Psi + k/2 K2,
  *     T_C = Psi + k K3 (T_C in the accumulator's buffer); stage 4 forms Psi' = Psi +
  *     ((T_A - Psi) + 2 (T_B - Psi) + (T_C - Psi))/3 + k/6 K4 (the accumulator is never

@@ -5,13 +5,14 @@ The paper counts operations and storage of the Laplacian and of one RK4 step for
 non-compact scheme and the 2SHOC single-storage ("1X") and multi-storage ("2X"/"3X") forms.
 Here each realisation in the library is timed on one B200 at a paper-sized workload:
 
-  fused-13  variant 0: one kernel per stage, wide 2SHOC form (= the non-compact stencil in the
-            interior), write-light combine in 2D/3D (13 field transfers per point-step)
-  fused-13r variant 6: as fused-13 with the reconstructed accumulator (13 transfers)
-  fused-16  variant 2: as fused-13 with the explicit accumulator (16 transfers)
+  fused-12  variant 0: one kernel per stage, wide 2SHOC form (= the non-compact stencil in the
+            interior), carried-sum combine (12 field transfers per point-step)
+  fused-13  variant 5: as fused-12 with the write-light combine (13 transfers)
+  fused-13r variant 6: as fused-12 with the reconstructed accumulator (13 transfers)
+  fused-16  variant 2: as fused-12 with the explicit accumulator (16 transfers)
   2k-1X     variant 1: the paper's single-storage two-step scheme, D stored (`2d2shocs1/2`)
   2k-MS     variant 3: the paper's multi-storage scheme, D_d per axis stored (`*2shocMs1/2`)
-  CD        scheme CD through fused-13 (`uttmp`, the 2nd-order comparison scheme)
+  CD        scheme CD through fused-12 (`uttmp`, the 2nd-order comparison scheme)
   pairs     variant 4: two stages per pass (temporal blocking, stage_pair.cuh)
 
   python scripts/cost_tables.py                 # timing -> JSON lines on stdout
@@ -33,7 +34,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
-ROWS = [("fused-13", 0, "2shoc"), ("fused-13r", 6, "2shoc"), ("fused-16", 2, "2shoc"), ("2k-1X", 1, "2shoc"),
+ROWS = [("fused-12", 0, "2shoc"), ("fused-13", 5, "2shoc"), ("fused-13r", 6, "2shoc"), ("fused-16", 2, "2shoc"), ("2k-1X", 1, "2shoc"),
         ("2k-MS", 3, "2shoc"), ("CD", 0, "cd"), ("pairs", 4, "2shoc")]
 
 # paper's static counts (Tables 3-5): (Laplacian ops, Laplacian storage, RK4 ops, RK4 storage)
@@ -52,7 +53,7 @@ def workloads():
 
 
 def rows_for(dims):
-    return [r for r in ROWS if not (dims == 1 and r[1] in (3, 4, 6))]  # 1D: MS == 1X, 0 == 6; pairs 2D/3D
+    return [r for r in ROWS if not (dims == 1 and r[1] in (3, 4, 6))]  # 1D: MS == 1X; pairs 2D/3D
 
 
 def run(ncu: bool, steps: int, reps: int, only):
