@@ -32,7 +32,7 @@ def run(work, dtype, steps, variant=0, synthetic=False):
     S_b = 8 if dtype == "c64" else 16
     r = {"config": work["name"], "dtype": dtype, "variant": {0: "fused", 1: "two_kernel", 4: "stage_pairs"}[variant], "grid": g["n"][:dims],
          "steps": steps, "ms_per_step": ms / steps, "pt_steps_s": npts * steps / ms * 1e3,
-         "alg_GBs_13S": npts * steps * 13 * S_b / ms / 1e6, "alg_GBs_16S": npts * steps * 16 * S_b / ms / 1e6,
+         "alg_GBs_12S": npts * steps * 12 * S_b / ms / 1e6, "alg_GBs_16S": npts * steps * 16 * S_b / ms / 1e6,
          "launches": S.last_launch_count}
     S.close(); del psi; torch.cuda.empty_cache()
     return r
