@@ -244,6 +244,14 @@ nlse2shoc_status nlse2shoc_set_scheme(nlse2shoc_t, int scheme);
  *                    finish together; 0 = equal chunks.  Bit-identical.
  * Single-slab and sharded rk4 calls keep their instantiated CUDA graph and replay it in
  * later calls with the same psi pointer and dt (any set_* call drops it).
+ *  CHECK_EVERY   [0] failure detection (an explicit scheme past its
+ *                    stability bound blows up): n > 0 makes rk4 scan Psi for NaN / Inf after
+ *                    every n steps (each scan syncs the stream; sharded: collective) and
+ *                    return ENONFINITE as soon as one is found, nlse2shoc_last_error() naming
+ *                    the number of steps taken; Psi then holds the state at that step.  0 = no
+ *                    scan, rk4 stays asynchronous.  The arithmetic is unchanged (n steps at a
+ *                    time replay the same step graph).  EUNSUPPORTED in nlse2shoc_rk4_padded
+ *                    when the pitch differs from N_x (the scan reads the dense layout).
  * EINVAL for an unknown option or a negative value.                                     */
 typedef enum {
   NLSE2SHOC_OPT_CUDA_GRAPH = 0,
@@ -254,7 +262,8 @@ typedef enum {
   NLSE2SHOC_OPT_ZCHUNKS = 5,
   NLSE2SHOC_OPT_TILE_SCHEDULE = 6,
   NLSE2SHOC_OPT_FUSED_EXCHANGE = 7,
-  NLSE2SHOC_OPT_TAIL_CHUNKS = 8
+  NLSE2SHOC_OPT_TAIL_CHUNKS = 8,
+  NLSE2SHOC_OPT_CHECK_EVERY = 9
 } nlse2shoc_option;
 nlse2shoc_status nlse2shoc_set_option(nlse2shoc_t, int option, int64_t value);
 

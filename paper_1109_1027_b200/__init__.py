@@ -121,7 +121,7 @@ def nlse2shoc_check_finite(H, psi, stream=None):
 
 
 OPTIONS = {"cuda_graph": 0, "overlap": 1, "resident_1d": 2, "reverse_order": 3, "lean_steps": 4, "zchunks": 5,
-           "tile_schedule": 6, "fused_exchange": 7, "tail_chunks": 8}
+           "tile_schedule": 6, "fused_exchange": 7, "tail_chunks": 8, "check_every": 9}
 
 
 def nlse2shoc_set_option(H, option, value: int):
@@ -218,7 +218,8 @@ class Solver:
 
     def set_option(self, option, value: int):
         """Execution-path option (include/nlse2shoc.h nlse2shoc_option): 'cuda_graph',
-        'overlap', 'resident_1d', 'reverse_order', 'lean_steps', 'zchunks', 'tile_schedule'."""
+        'overlap', 'resident_1d', 'reverse_order', 'lean_steps', 'zchunks', 'tile_schedule',
+        'fused_exchange', 'tail_chunks', 'check_every'."""
         nlse2shoc_set_option(self._h, option, value)
 
     def connect_peers(self, group=None):

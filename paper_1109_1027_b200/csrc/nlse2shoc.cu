@@ -120,6 +120,7 @@ struct nlse2shoc_s {
   int opt_graph = 1, opt_overlap = 1, opt_resident = 1, opt_reverse = 1, opt_lean = 3, opt_zchunks = 0;
   int opt_sched = -1;         // -1: automatic (dynamic)
   int opt_tail = 1;           // option TAIL_CHUNKS
+  int opt_check_every = 0;    // option CHECK_EVERY (steps between non-finite scans; 0: none)
   std::map<uint64_t, ZLayout> zmemo;  // z-chunk layouts chosen so far (zlayout_dynamic)
   unsigned *sched = nullptr;  // dynamic tile schedule counters {next tile, finished CTAs}
   // one instantiated RK4-step graph, reused by later calls with the same psi, dt and settings
@@ -1512,6 +1513,7 @@ nlse2shoc_status nlse2shoc_set_option(nlse2shoc_t H, int option, int64_t value) 
     case NLSE2SHOC_OPT_TILE_SCHEDULE: H->opt_sched = v >= 2 ? -1 : v; break;
     case NLSE2SHOC_OPT_FUSED_EXCHANGE: H->opt_fused = v != 0; break;
     case NLSE2SHOC_OPT_TAIL_CHUNKS: H->opt_tail = v != 0; break;
+    case NLSE2SHOC_OPT_CHECK_EVERY: H->opt_check_every = v; break;
     default: return fail(NLSE2SHOC_EINVAL, "unknown option");
   }
   ++H->gen;
@@ -1608,6 +1610,30 @@ static nlse2shoc_status rk4_entry(nlse2shoc_t H, void *psi, double dt, int64_t n
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   reset_launches(H);
   if (nsteps == 0) return NLSE2SHOC_OK;
+  if (H->opt_check_every > 0) {
+    // failure detection (option CHECK_EVERY): chunks of n steps, each followed by a scan of Psi
+    if (padded && H->pitch != H->nx) return fail(NLSE2SHOC_EUNSUPPORTED, "CHECK_EVERY scans the dense layout");
+    int64_t launches = 0;
+    for (int64_t done = 0; done < nsteps;) {
+      const int64_t n = std::min<int64_t>(H->opt_check_every, nsteps - done);
+      View v;
+      void *work = nullptr;
+      TRY(make_view(H, psi, v, &work, st, padded));
+      TRY(run_rk4(v, dt, n, st));
+      TRY(unstage(H, psi, work, st));
+      launches += nlse2shoc_last_launch_count(H);
+      done += n;
+      double r[3];
+      if (H->dtype == NLSE2SHOC_C64) TRY(reduce_N<float>(H, psi, r, st));
+      else TRY(reduce_N<double>(H, psi, r, st));
+      if (r[2] > 0)
+        return fail(NLSE2SHOC_ENONFINITE, std::to_string(int64_t(r[2])) + " non-finite values after step " +
+                                              std::to_string(done) + " of " + std::to_string(nsteps));
+      reset_launches(H);
+    }
+    H->launches = launches;
+    return NLSE2SHOC_OK;
+  }
   View v;
   void *work = nullptr;
   TRY(make_view(H, psi, v, &work, st, padded));

@@ -684,3 +684,37 @@ def test_carried_sum_keeps_any_constant_to_the_bit(dims, n, dtype):
         S2.rk4(g, 0.5 * S2.stability_bound(g), 5)
         outs.append(g.cpu())
     assert torch.isfinite(torch.view_as_real(outs[0])).all() and torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("shard", [None, {"loopback": 2}])
+def test_check_every_detects_blow_up(shard):
+    """Failure detection: past the stability bound the explicit scheme
+    blows up; with option CHECK_EVERY rk4 stops at the first scan that finds a non-finite value
+    and names the step, and below the bound the chunked call gives the bits of the plain one."""
+    import re
+
+    import paper_1109_1027_b200 as nl
+    from paper_1109_1027_b200 import _lib
+
+    w = _small(3, (70, 30, 24), "dirichlet", "c64", "harmonic")
+    psi = H.psi0_host(w, "c64")
+    S = nl.solver_from_work(w, "c64", shard=shard)
+    kmax = S.stability_bound(_dev(psi))
+    a = _dev(psi)
+    S.rk4(a, 0.8 * kmax, 23)
+    S.set_option("check_every", 5)
+    b = _dev(psi)
+    S.rk4(b, 0.8 * kmax, 23)
+    assert torch.equal(a, b)
+    c = _dev(psi)
+    with pytest.raises(nl.NLSE2SHOCError) as ei:
+        S.rk4(c, 3.0 * kmax, 2000)
+    assert ei.value.status == _lib.ENONFINITE
+    m = re.search(r"after step (\d+) of 2000", str(ei.value))
+    assert m and int(m.group(1)) % 5 == 0 and int(m.group(1)) < 2000
+    assert not torch.isfinite(torch.view_as_real(c)).all()
+    S.set_option("check_every", 0)  # off again: the call is asynchronous and reports nothing
+    d = _dev(psi)
+    S.rk4(d, 3.0 * kmax, int(m.group(1)))
+    assert not torch.isfinite(torch.view_as_real(d)).all()
+    S.close()
