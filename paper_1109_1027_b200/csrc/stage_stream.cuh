@@ -75,19 +75,12 @@ template <int SLOT_B, int PT_B> struct Rings {
 // chosen by a sweep over (TY, warps, rows/warp) on C4 (scripts/sweep.py; 28 rows / 14 warps
 // until the exact-cancellation stencil R30 made the stage more issue-bound: v18 A/B C4
 // 4.864e10 (28/14) vs 4.895e10 (24/12) vs 4.799e10 (24 rows, 8 warps x 3 rows)).
-#if defined(NLSE_TILE3F_128x12)  // experiment: 1 KB rows (DRAM page locality), 12 rows
-template <> struct Cfg<3, float> : Rings<132 * (12 + 4) * 8, 128 * 12 * 8> {
-  static constexpr int TX = 128, TY = 12, PPX = 2, RPW = 2, NCW = 12, NBOX = 1, NBOXP = 1, W = 132;
-};
-#elif defined(NLSE_TILE3F_128x16)  // experiment: 1 KB rows, 16 rows, 16 consumer warps
-template <> struct Cfg<3, float> : Rings<132 * (16 + 4) * 8, 128 * 16 * 8> {
-  static constexpr int TX = 128, TY = 16, PPX = 2, RPW = 2, NCW = 16, NBOX = 1, NBOXP = 1, W = 132;
-};
-#else
+// (r2: 128 x 12 tiles, 1 KB rows: the two-write stage 2 gains 2 % (6.42 TB/s), stages 1, 3, 4 lose
+// 3-8 %, C4 7.70 -> 7.95 ms/step; 128 x 16 with 16 warps spills at 96 registers;
+// profiles/r02/ab_tile_128x12.jsonl)
 template <> struct Cfg<3, float> : Rings<68 * (24 + 4) * 8, 64 * 24 * 8> {
   static constexpr int TX = 64, TY = 24, PPX = 2, RPW = 2, NCW = 12, NBOX = 1, NBOXP = 1, W = 68;
 };
-#endif
 // 3D complex128 tiles: 32 x 32, 8 consumer warps x 4 rows (sweep on C5W c128, ms/step:
 // 32x28/14 warps x 2 rows 4.38, 32x32/8x4 4.24, 32x40/10x4 4.25, 32x20/10x2 4.29, 32x24/12x2 4.32)
 template <> struct Cfg<3, double> : Rings<36 * (32 + 4) * 16, 32 * 32 * 16> {
