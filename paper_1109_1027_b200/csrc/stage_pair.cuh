@@ -1,6 +1,6 @@
 // stage_pair.cuh — temporal blocking: two RK4 stages per pass over HBM.
 //
-// The four stage launches of one step (stage_stream.cuh) move 13 field transfers per
+// The four stage launches of one step (stage_stream.cuh) move 12-13 field transfers per
 // point-step.  Here one launch runs a PAIR of stages over a (column, z-chunk) tile:
 //
 //   pair A (stages 1+2):  reads Psi (halo 4)                -> writes acc, T_B

@@ -8,9 +8,9 @@
 //     ghost = h_d^2 D_d(b) + 2 Psi_b - Psi_{b+n}, D_d(b) = lambda_b - sum_{e!=d} delta_e^2 Psi_b,
 //     computed in shared memory by the CTA that needs it (no extra pass, no padded arrays);
 //   * F = i(a Lap + (s|Psi|^2 - V) Psi) with the Psi_t boundary rule;
-//   * the RK4 stage combine in Psi-space accumulator form: 13 field transfers
-//     per point-step with the reconstructed accumulator (default), 16 with the explicit one;
-//     the paper's listing costs 17.
+//   * the RK4 stage combine in Psi-space form: 12 field transfers per point-step
+//     with the carried sum (default), 13 with the write-light or reconstructed accumulator,
+//     16 with the explicit one; the paper's listing costs 17.
 //
 // Data movement: the slowest axis ("z"; y in 2D) is streamed.  A producer warp issues TMA
 // boxes of one plane (tile + 2-cell halo) into a ring of shared-memory slots guarded by
@@ -96,6 +96,9 @@ template <> struct Cfg<2, float> {
   static constexpr int TX = 1024, TY = 1, PPX = 4, RPW = 1, NCW = 8, NBOX = 5, NBOXP = 4, W = 1040;
   static constexpr int RT0 = 24, RT1 = 12, RP1 = 12, RT2 = 10, RP2 = 7, RT3 = 10, RP3 = 4;
 };
+// (r2: 1024-point rows with 16 consumer warps x 2 points for complex128: 96 registers with
+// 150-350 B of spills and half the ring depth, C3 2.21 -> 2.90 ms/step;
+// profiles/r02/ab_tile2d_1024x16w.jsonl)
 template <> struct Cfg<2, double> {
   static constexpr int TX = 512, TY = 1, PPX = 2, RPW = 1, NCW = 8, NBOX = 5, NBOXP = 4, W = 520;
   static constexpr int RT0 = 24, RT1 = 12, RP1 = 12, RT2 = 10, RP2 = 7, RT3 = 10, RP3 = 4;

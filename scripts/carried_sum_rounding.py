@@ -64,8 +64,6 @@ def step(re,im,variant):
         if variant==73: # everything of the carry exact (f64)
             A2e=(re.astype(np.float64)+np.float64(W)*d[0]-dt/3*t[1].astype(np.float64), im.astype(np.float64)+np.float64(W)*d[1]+dt/3*t[0].astype(np.float64))
             Q=(A2e[0]-np.float64(W)*re,A2e[1]-np.float64(W)*im)
-    if variant==8:  # carry increment-only?? needs psi in stage 4 (13 transfers) -- reference for accuracy
-        pass
     if variant in (9,10):
         d=((TA[0]-re).astype(f32),(TA[1]-im).astype(f32))
         tt=(fma(re,f32(2),d[0]),fma(im,f32(2),d[1]))

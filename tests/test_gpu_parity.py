@@ -366,7 +366,7 @@ def _core_box_work(w, lo, cnt):
 def test_C4_core_box_full_step_count(dtype, variant):
     """C4 at its stated step count (100) on a 96^3 box around the ring core with C4's own
     spacing (SURVEY A7 analogue): the whole-field parity the north star states, for the
-    default 13-transfer form and the explicit-accumulator form."""
+    default carried-sum form, the 13-transfer forms and the explicit-accumulator form."""
     w = configs.C4()
     lo, cnt = [336, 336, 336], [96, 96, 96]
     wc = _core_box_work(w, lo, cnt)
