@@ -98,19 +98,12 @@ template <> struct Cfg<2, float> {
 };
 // (r2: 1024-point rows with 16 consumer warps x 2 points for complex128: 96 registers with
 // 150-350 B of spills and half the ring depth, C3 2.21 -> 2.90 ms/step;
-// profiles/r02/ab_tile2d_1024x16w.jsonl)
-#ifdef NLSE_2D_C128_OCC2  // experiment: two CTAs per SM (<= 112 registers, half-depth rings)
-template <> struct Cfg<2, double> {
-  static constexpr int TX = 512, TY = 1, PPX = 2, RPW = 1, NCW = 8, NBOX = 5, NBOXP = 4, W = 520;
-  static constexpr int RT0 = 12, RT1 = 6, RP1 = 6, RT2 = 5, RP2 = 3, RT3 = 5, RP3 = 2;
-  static constexpr int MINB = 2;
-};
-#else
+// profiles/r02/ab_tile2d_1024x16w.jsonl; two CTAs per SM with half-depth rings: the same 96
+// registers and spills, 2.21 -> 2.69; ab_2d_c128_two_ctas.jsonl)
 template <> struct Cfg<2, double> {
   static constexpr int TX = 512, TY = 1, PPX = 2, RPW = 1, NCW = 8, NBOX = 5, NBOXP = 4, W = 520;
   static constexpr int RT0 = 24, RT1 = 12, RP1 = 12, RT2 = 10, RP2 = 7, RT3 = 10, RP3 = 4;
 };
-#endif
 
 template <typename R> struct StageParams {
   int nx, ny, nz;        // local extents: x, y (1 in 2D), streamed axis (local slab)
@@ -160,12 +153,8 @@ template <typename R> struct StageParams {
   cplx<R> *out_acc;      // accumulator (stages 1-3)
 };
 
-template <typename C, typename = void> struct MinBlocks { static constexpr int value = 1; };
-template <typename C> struct MinBlocks<C, std::void_t<decltype(C::MINB)>> { static constexpr int value = C::MINB; };
-
 template <int DIMS, typename R> struct Layout {
   using C = Cfg<DIMS, R>;
-  static constexpr int MINB = MinBlocks<C>::value;  // CTAs per SM the kernel is compiled for
   static constexpr int HY = DIMS == 3 ? 2 : 0;
   static constexpr int SROWS = C::TY + 2 * HY;
   static constexpr int SLOT = C::W * SROWS;                // complex per T slot
@@ -305,7 +294,7 @@ __device__ __forceinline__ void lds_run(const cplx<R> *p, cplx<R> *out) {
 }
 
 template <int DIMS, typename R, int MODE>
-__global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, Layout<DIMS, R>::MINB)
+__global__ void __launch_bounds__(Layout<DIMS, R>::NTHREADS, 1)
     stage_stream_kernel(const __grid_constant__ CUtensorMap tm_T, const __grid_constant__ CUtensorMap tm_lo,
                         const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_psi,
                         const __grid_constant__ CUtensorMap tm_acc, const __grid_constant__ CUtensorMap tm_t3,
