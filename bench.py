@@ -345,6 +345,8 @@ def run_ours(args):
     key = f"{wl}_{dtype}"
     if tr and tr.get("workload") in (wl, key) and tr.get("dram_bytes_per_point_stage"):
         traffic = tr["dram_bytes_per_point_stage"] * pts_local
+    elif tr and key in tr.get("workloads", {}):
+        traffic = tr["workloads"][key]["dram_bytes_per_point_stage"] * pts_local
     clocks = clk.summary()
 
     if rank == 0:
