@@ -83,6 +83,8 @@ template <> struct Cfg<3, float> : Rings<68 * (24 + 4) * 8, 64 * 24 * 8> {
 };
 // 3D complex128 tiles: 32 x 32, 8 consumer warps x 4 rows (sweep on C5W c128, ms/step:
 // 32x28/14 warps x 2 rows 4.38, 32x32/8x4 4.24, 32x40/10x4 4.25, 32x20/10x2 4.29, 32x24/12x2 4.32)
+// (r2: 16 consumer warps x 2 rows instead of 8 x 4: 96 registers with 540-840 B of spills, C5W
+// c128 3.98 -> 4.86 ms/step; profiles/r02/ab_16_warps.jsonl)
 template <> struct Cfg<3, double> : Rings<36 * (32 + 4) * 16, 32 * 32 * 16> {
   static constexpr int TX = 32, TY = 32, PPX = 1, RPW = 4, NCW = 8, NBOX = 1, NBOXP = 1, W = 36;
 };
@@ -92,6 +94,7 @@ template <> struct Cfg<3, double> : Rings<36 * (32 + 4) * 16, 32 * 32 * 16> {
 // 1.79 / 3.34, 1024 / 512-wide rows with 4 / 2 points per thread 1.49 / 2.67 (kept), the
 // same with 16 consumer warps 1.47 / 2.69, 2048 / 1024-wide rows 2.16 / 3.48 (spills).
 // Wider rows amortise the per-row barrier round trip over more bytes.
+// (r2, complex64: 16 consumer warps x 2 points instead of 8 x 4: C3 c64 1.194 -> 1.219 ms/step)
 template <> struct Cfg<2, float> {
   static constexpr int TX = 1024, TY = 1, PPX = 4, RPW = 1, NCW = 8, NBOX = 5, NBOXP = 4, W = 1040;
   static constexpr int RT0 = 24, RT1 = 12, RP1 = 12, RT2 = 10, RP2 = 7, RT3 = 10, RP3 = 4;
@@ -100,8 +103,13 @@ template <> struct Cfg<2, float> {
 // 150-350 B of spills and half the ring depth, C3 2.21 -> 2.90 ms/step;
 // profiles/r02/ab_tile2d_1024x16w.jsonl; two CTAs per SM with half-depth rings: the same 96
 // registers and spills, 2.21 -> 2.69; ab_2d_c128_two_ctas.jsonl)
+// complex128 rows: one point per thread, 16 consumer warps (r2; 8 warps x 2 points had a
+// 32-byte thread stride, i.e. 2-way bank conflicts on every 128-bit shared-memory load, and 9
+// warps per SM at 168 registers: stage 1 ran at 0.68 of the copy bandwidth.  One point per
+// thread is conflict-free, fits 96 registers without spills and doubles the warps: stage 1
+// 478 -> 420 us, C3 2.209 -> 2.145 ms/step; profiles/r02/ab_16_warps.jsonl)
 template <> struct Cfg<2, double> {
-  static constexpr int TX = 512, TY = 1, PPX = 2, RPW = 1, NCW = 8, NBOX = 5, NBOXP = 4, W = 520;
+  static constexpr int TX = 512, TY = 1, PPX = 1, RPW = 1, NCW = 16, NBOX = 5, NBOXP = 4, W = 520;
   static constexpr int RT0 = 24, RT1 = 12, RP1 = 12, RT2 = 10, RP2 = 7, RT3 = 10, RP3 = 4;
 };
 
