@@ -78,6 +78,8 @@ template <int SLOT_B, int PT_B> struct Rings {
 // (r2: 128 x 12 tiles, 1 KB rows: the two-write stage 2 gains 2 % (6.42 TB/s), stages 1, 3, 4 lose
 // 3-8 %, C4 7.70 -> 7.95 ms/step; 128 x 16 with 16 warps spills at 96 registers;
 // profiles/r02/ab_tile_128x12.jsonl)
+// (r2, carried-sum stage mix: 64 x 28 with 14 warps x 2 rows 7.73-7.97 against 7.59-7.80 ms/step;
+// 64 x 16 with 16 warps x 1 row, 96 registers: 8.48-8.54; profiles/r02/ab_tile3d_C4.jsonl)
 template <> struct Cfg<3, float> : Rings<68 * (24 + 4) * 8, 64 * 24 * 8> {
   static constexpr int TX = 64, TY = 24, PPX = 2, RPW = 2, NCW = 12, NBOX = 1, NBOXP = 1, W = 68;
 };
