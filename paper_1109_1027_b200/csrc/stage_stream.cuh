@@ -87,6 +87,8 @@ template <> struct Cfg<3, float> : Rings<68 * (24 + 4) * 8, 64 * 24 * 8> {
 // 32x28/14 warps x 2 rows 4.38, 32x32/8x4 4.24, 32x40/10x4 4.25, 32x20/10x2 4.29, 32x24/12x2 4.32)
 // (r2: 16 consumer warps x 2 rows instead of 8 x 4: 96 registers with 540-840 B of spills, C5W
 // c128 3.98 -> 4.86 ms/step; profiles/r02/ab_16_warps.jsonl)
+// (r2 re-check with the carried-sum stage mix, C5W c128 median ms/step: 32 x 24 / 12 warps x 2 rows
+// 4.02, 32 x 36 / 12 x 3 4.40, this one 4.00-4.05; profiles/r02/ab_tile3d_C5Wc128.jsonl)
 template <> struct Cfg<3, double> : Rings<36 * (32 + 4) * 16, 32 * 32 * 16> {
   static constexpr int TX = 32, TY = 32, PPX = 1, RPW = 4, NCW = 8, NBOX = 1, NBOXP = 1, W = 36;
 };
