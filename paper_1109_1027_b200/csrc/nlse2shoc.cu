@@ -1679,17 +1679,23 @@ nlse2shoc_status nlse2shoc_set_workspace(nlse2shoc_t H, void *dev, size_t bytes)
   CUDA_TRY(cudaDeviceSynchronize());  // nothing in flight may still use the old fields
   graph_drop(H);
   const size_t f = nlse2shoc_stage_workspace_bytes(H) / 3, own = size_t(H->local_elems) * H->S;
+  // release the handle's own fields first, so that an error below never leaves a field the
+  // handle would free pointing into the caller's memory
+  if (!H->ws_external)
+    for (Field *fl : {&H->TA, &H->TB, &H->acc})
+      if (fl->ptr) {
+        void *p = fl->ptr;
+        fl->ptr = nullptr;
+        H->bytes -= own;
+        CUDA_TRY(dev_free(H, p));
+      }
+  H->ws_external = true;
+  ++H->gen;
   int i = 0;
   for (Field *fl : {&H->TA, &H->TB, &H->acc}) {
-    if (!H->ws_external && fl->ptr) {
-      CUDA_TRY(dev_free(H, fl->ptr));
-      H->bytes -= own;
-    }
     fl->ptr = reinterpret_cast<char *>(dev) + size_t(i++) * f;
     TRY(encode_maps(H, *fl));
   }
-  H->ws_external = true;
-  ++H->gen;
   return NLSE2SHOC_OK;
 }
 
