@@ -168,14 +168,25 @@ def host_info():
     return {"cpu_model": model, "sockets": len(sockets) or None, "nproc": os.cpu_count()}
 
 
+def calibrated_sample(work, box, seconds, max_steps=1000):
+    """Oracle sample of about `seconds` of CPU work: a 3-step call on the box to estimate the
+    rate, then as many steps (2 ... max_steps) in one call as fit the budget."""
+    oracle_sample(work, 1, box=box)  # first touch: thread pool, page faults
+    _, t3, _ = oracle_sample(work, 3, box=box)
+    steps = int(min(max_steps, max(2, round(seconds / max(t3 / 3, 1e-6)))))
+    pts, t, desc = oracle_sample(work, steps, box=box)
+    return pts * steps, t, desc
+
+
 def cpu_baseline_line(work, box):
-    """The oracle on all host cores (box^3 sample) and on one core (a smaller sample)."""
+    """The oracle as it stands on all host cores (a bounded sample of the workload: a centred
+    box^3 box for about 12 s of CPU work) and on one core (a smaller box, about 4 s)."""
     import oracle
 
     nth = oracle.set_threads(0)
-    pts, tcpu, desc = oracle_sample(work, 1, box=box)
+    pts, tcpu, desc = calibrated_sample(work, box, 12.0)
     oracle.set_threads(1)
-    p1, t1, d1 = oracle_sample(work, 1, box=max(16, box // 2))
+    p1, t1, d1 = calibrated_sample(work, max(16, box // 2), 4.0)
     oracle.set_threads(nth)
     return {"value": pts / tcpu, "unit": UNIT, "cores": nth, "kind": "oracle", "sample": desc,
             "value_1core": p1 / t1, "sample_1core": d1, **host_info()}
@@ -194,13 +205,16 @@ def run_reference(args):
     wl = args.workload
     work = workload(wl, ws)
     dtype = args.dtype or DTYPE_DEFAULT.get(wl, "c64")
-    box = int(os.environ.get("NLSE_REF_BOX", "96"))
+    # one bench step of the reference arm = one oracle call of REF_STEPS RK4 steps on a centred
+    # box^3 box of the workload (a bounded sample: about a second of CPU work per bench step)
+    box = int(os.environ.get("NLSE_REF_BOX", "128"))
+    ref_steps = int(os.environ.get("NLSE_REF_STEPS", "32"))
     for _ in range(args.warmup):
         oracle_sample(work, 1, box=min(box, 48), dtype=dtype)
     tot_pts, tot_t, desc = 0, 0.0, ""
     for _ in range(args.steps):
-        pts, t, desc = oracle_sample(work, 1, box=box, dtype=dtype)
-        tot_pts += pts
+        pts, t, desc = oracle_sample(work, ref_steps, box=box, dtype=dtype)
+        tot_pts += pts * ref_steps
         tot_t += t
     value = tot_pts / tot_t
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
@@ -377,7 +391,7 @@ def run_ours(args):
             "clocks": clocks,
         }
         if ws == 1 and not args.no_cpu_baseline and wl == "C4":
-            line["cpu_baseline"] = cpu_baseline_line(work, int(os.environ.get("NLSE_REF_BOX", "96")))
+            line["cpu_baseline"] = cpu_baseline_line(work, int(os.environ.get("NLSE_REF_BOX", "128")))
         print(json.dumps(line), flush=True)
     S.close()
     if dist is not None:
