@@ -302,8 +302,8 @@ def test_C3_full_size_200_steps():
 def test_C4_full_size_25_steps():
     """C4 (768^3 c64, bench config) after 25 of its 100 steps on boxes at a corner, the ring
     core, an x-face, a z-face edge and the far corner (margin 200).  The 100-step full-grid
-    comparison needs ~20 min of oracle time on the GPU box: scripts/c4_full_parity.py, result
-    in profiles/r02/."""
+    comparison needs ~11 min of oracle time on the GPU box (scripts/full_grid_parity.py C4 c64;
+    result in profiles/r02/)."""
     w = configs.C4()
     n = 768
     T = [([0, 0, 0], [20, 18, 16]), ([370, 380, 376], [24, 20, 16]), ([0, 300, 500], [12, 24, 20]),
