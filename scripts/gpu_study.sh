@@ -1,6 +1,8 @@
 # study captures: launch list and --set full of one step's four stage launches for a config
 mkdir -p gpurun_out
-for cfg in "C3 c128 67108864" "C2 c128 4194304"; do
+# usage: bash scripts/gpu_study.sh ["CFG DTYPE NPOINTS" ...]
+if [ $# -eq 0 ]; then set -- "C3 c128 67108864" "C2 c128 4194304"; fi
+for cfg in "$@"; do
   set -- $cfg
   tag=$1_$2
   timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 40 --csv --log-file gpurun_out/study_launches_$tag.csv python scripts/one_step.py $1 $2 2 > /dev/null 2>&1
